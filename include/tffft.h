@@ -1,0 +1,122 @@
+/* tffft — transpose-free slab 3D real FFT for NVIDIA B200 (sm_100a).
+ *
+ * C ABI of the hot path.  Every pointer passed to a transform is a DEVICE
+ * pointer on the plan's device; every transform call is asynchronous on the
+ * given cudaStream_t (passed as void*, NULL = legacy default stream) and
+ * returns an int status.  Status codes map 1:1 onto the reference's
+ * exception classes (reference pkg/src/slabfft/errors.py:4-33); the message
+ * of the last failure on the calling thread is in tffft_last_error().
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   tffft_plan_create      <- slabfft.dfft.plan            pkg/src/slabfft/dfft.py:93-145
+ *   tffft_forward          <- slabfft.dfft.forward         pkg/src/slabfft/dfft.py:148-176
+ *   tffft_inverse          <- slabfft.dfft.inverse         pkg/src/slabfft/dfft.py:179-215
+ *   tffft_comm_init_local  <- slabfft.transport.make_communicators  transport.py:425-430
+ *   tffft_comm_init_rank   <- (MPI communicator; NCCL over NVLink)
+ *   tffft_stage_times      <- FftPlan.timers_us            dfft.py:84-90, 173-175
+ *   tffft_counters         <- CopyCounter.snapshot         transport.py:97-114
+ *   tffft_consistency      <- FftPlan.last_imag_residue + ConsistencyError  dfft.py:73,211; kernels.py:212-239
+ *   tffft_exchange_schedule<- ExchangePlan STRIDED descriptors  exchange.py:106-121
+ */
+#ifndef TFFFT_H
+#define TFFFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py) */
+enum {
+  TFFFT_OK = 0,
+  TFFFT_ERR_SIZE = 1,          /* SizeError          errors.py:8-9   */
+  TFFFT_ERR_LAYOUT = 2,        /* LayoutError        errors.py:12-13 */
+  TFFFT_ERR_CONFIGURATION = 3, /* ConfigurationError errors.py:16-17 */
+  TFFFT_ERR_CONTRACT = 4,      /* ContractError      errors.py:20-21 */
+  TFFFT_ERR_PROTOCOL = 5,      /* ProtocolError      errors.py:24-25 */
+  TFFFT_ERR_TRANSPORT = 6,     /* TransportError     errors.py:28-29 */
+  TFFFT_ERR_CONSISTENCY = 7,   /* ConsistencyError   errors.py:32-33 */
+  TFFFT_ERR_CUDA = 8,          /* CUDA runtime failure (SlabFftError) */
+  TFFFT_ERR_INTERNAL = 9
+};
+
+/* element precision of a plan: real element f64 (complex128) or f32 (complex64) */
+enum { TFFFT_F64 = 0, TFFFT_F32 = 1 };
+
+/* exchange pattern (transport.py:51-53) */
+enum { TFFFT_PAIRWISE = 0, TFFFT_COLLECTIVE = 1 };
+
+typedef struct tffft_comm_s* tffft_comm_t;
+typedef struct tffft_plan_s* tffft_plan_t;
+
+const char* tffft_last_error(void);
+int tffft_version(void);
+
+/* --- communicators ------------------------------------------------------ */
+/* NCCL unique id (128 bytes) for tffft_comm_init_rank; call on one rank and broadcast. */
+int tffft_get_unique_id(uint8_t out[128]);
+/* One process (or thread) per GPU: NCCL communicator over NVLink/NVSwitch. */
+int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tffft_comm_t* comm);
+/* p endpoints sharing one in-process fabric on ONE device (the reference's
+ * in-process multi-rank fabric, transport.py:188-302).  Each endpoint is
+ * driven by its own host thread; forward/inverse are collectives. */
+int tffft_comm_init_local(int p, int device, tffft_comm_t* comms);
+int tffft_comm_rank(tffft_comm_t comm, int* rank);
+int tffft_comm_size(tffft_comm_t comm, int* p);
+int tffft_comm_device(tffft_comm_t comm, int* device);
+/* Abort: wakes every rank blocked in the fabric with TFFFT_ERR_TRANSPORT (transport.py:209-219). */
+int tffft_comm_abort(tffft_comm_t comm);
+int tffft_comm_destroy(tffft_comm_t comm);
+
+/* --- plans -------------------------------------------------------------- */
+/* n0, n1, n2: powers of two in [2, 4096]; p = comm size must divide n0 and n1
+ * (layout.py:83-93).  pattern: TFFFT_PAIRWISE (chunk-granular in-place landing). */
+int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm_t comm,
+                      tffft_plan_t* plan);
+/* device bytes owned by the plan (staging, twiddles, statistics) */
+int tffft_plan_workspace_bytes(tffft_plan_t plan, size_t* bytes);
+/* element counts: real slab n0/p*n1*n2 reals, spectral slab n1/p*n0*(n2/2+1) complex */
+int tffft_plan_sizes(tffft_plan_t plan, int64_t* real_elems, int64_t* spec_elems);
+int tffft_plan_destroy(tffft_plan_t plan);
+
+/* Forward r2c (collective).  real_in: (n0/p, n1, n2) row-major, not modified.
+ * spec_out: STRIDED_INPLACE spectral slab, logical (j, r, k) at
+ * (r % n0p)*n1*n2c + (r / n0p)*n1p*n2c + j*n2c + k (layout.py:189-198),
+ * value = unnormalised global bin (r, rank*n1p + j, k). */
+int tffft_forward(tffft_plan_t plan, const void* real_in, void* spec_out, void* stream);
+/* Inverse c2r (collective), normalised by 1/(n0 n1 n2).  spec_inout is
+ * consumed (overwritten) as in dfft.py:182-184; real_out: (n0/p, n1, n2). */
+int tffft_inverse(tffft_plan_t plan, void* spec_inout, void* real_out, void* stream);
+
+/* --- instrumentation ---------------------------------------------------- */
+/* enable CUDA-event stage timing (adds events, no host sync inside calls) */
+int tffft_set_timing(tffft_plan_t plan, int enable);
+/* accumulated {stage1, exchange, stage3} milliseconds since the last reset;
+ * synchronises on the recorded events */
+int tffft_stage_times(tffft_plan_t plan, double ms[3]);
+/* {bytes_packed, bytes_wire, bytes_unpacked} since the last reset */
+int tffft_counters(tffft_plan_t plan, uint64_t bytes[3]);
+int tffft_reset_instrumentation(tffft_plan_t plan);
+/* Hermitian consistency of the LAST inverse: synchronises on it, returns the
+ * largest discarded imaginary magnitude and TFFFT_ERR_CONSISTENCY when a plane
+ * violates the reference tolerance 1e-9*n2*max|X| (kernels.py:223-238). */
+int tffft_consistency(tffft_plan_t plan, double* residue);
+/* number of kernels this library launched on the plan since the last reset */
+int tffft_launch_count(tffft_plan_t plan, uint64_t* launches);
+
+/* --- host-only geometry (no GPU needed) ---------------------------------- */
+/* STRIDED exchange schedule of one rank: up to max_ops rows of
+ * {peer, send_offset, recv_offset, count} in complex elements, where
+ * send_offset indexes the staging buffer [q][i][j][k] and recv_offset the
+ * spectral slab.  Same list for forward and inverse (exchange.py:120-121). */
+int tffft_exchange_schedule(int n0, int n1, int n2, int p, int rank, int64_t* ops, int64_t max_ops,
+                            int64_t* nops);
+/* twiddle-table geometry of the radix schedule for length 2^log2n (for tests) */
+int tffft_radix_schedule(int log2n, int* radices, int* npasses);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFFFT_H */

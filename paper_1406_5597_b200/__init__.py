@@ -1,0 +1,18 @@
+"""paper_1406_5597_b200 — B200-native transpose-free slab 3D real FFT.
+
+Drop-in for the STRIDED path of the reference ``slabfft`` package
+(plan / forward / inverse with the STRIDED_INPLACE spectral layout); the
+transforms run in hand-written sm_100a CUDA (libtffft.so) behind a C ABI.
+"""
+
+from .dfft import (DTYPES, FftPlan, forward, gather_real, gather_spectral, inverse, plan,
+                   scatter_real, scatter_spectral)
+from .errors import (ConfigurationError, ConsistencyError, ContractError, CudaError, LayoutError,
+                     ProtocolError, SizeError, SlabFftError, TransportError)
+from .exchange import ExchangeOp, Strategy, exchange_schedule
+from .layout import (DistAxis, GlobalGrid, RealSlab, SlabLayout, SpectralSlab, SpectralTag,
+                     TwoLevelStride, column_stride_descriptor, owned_range, spectral_offset, validate)
+from .transport import (CommMode, CommPattern, CopyCounter, Endpoint, init_nccl_endpoint,
+                        make_communicators, run_spmd)
+
+__version__ = "0.1.0"

@@ -1,0 +1,268 @@
+// Register/shared-memory Stockham FFT engine for sm_100a.
+//
+// One length-N complex transform (N = 2^L, L <= 12) is owned by TPT = N/E
+// threads; each thread keeps E complex values in registers.  A transform runs
+// as P = ceil(L/4) radix passes (radix <= 16).  Pass 0 reads its operands
+// straight from global memory and the last pass writes its results straight
+// to global memory; the P-1 exchanges in between go through shared memory.
+//
+// Stockham autosort indexing (pass with radix R, Ns = product of earlier
+// radices, butterfly j in [0, N/R), k = j mod Ns):
+//   in : x[j + m*N/R]                        m = 0..R-1
+//   tw : v[m] *= exp(-+2*pi*i*m*k/(Ns*R))
+//   out: y[(j/Ns)*Ns*R + k + m*Ns]  = DFT_R(v)[m]
+// The first pass has Ns = 1 (no twiddles) and the last Ns*R = N, so its
+// outputs land in natural order at x[j + m*N/R].
+//
+// This replaces the reference's radix-2 bit-reversal DIT loop
+// (reference pkg/src/slabfft/kernels.py:134-161): same unnormalised DFT,
+// same sign convention (forward exp(-2*pi*i...), kernels.py:41-45).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tffft {
+
+// ---------------------------------------------------------------------------
+// radix schedule (shared by host table builder and device code)
+// ---------------------------------------------------------------------------
+constexpr int kMaxRadixBits = 4;
+constexpr int kMaxLog = 12;
+
+__host__ __device__ constexpr int num_passes(int L) {
+  return L == 0 ? 0 : (L + kMaxRadixBits - 1) / kMaxRadixBits;
+}
+__host__ __device__ constexpr int pass_bits(int L, int p) {
+  return (L / num_passes(L)) + (p < (L % num_passes(L)) ? 1 : 0);
+}
+__host__ __device__ constexpr int ept_bits(int L) { return L == 0 ? 0 : pass_bits(L, 0); }
+__host__ __device__ constexpr int ns_bits(int L, int p) {
+  return p == 0 ? 0 : ns_bits(L, p - 1) + pass_bits(L, p - 1);
+}
+// offset of pass p's twiddle block (passes >= 1 only); block p holds Ns*R entries
+__host__ __device__ constexpr int tw_offset(int L, int p) {
+  return p <= 1 ? 0 : tw_offset(L, p - 1) + (1 << (ns_bits(L, p - 1) + pass_bits(L, p - 1)));
+}
+__host__ __device__ constexpr int tw_total(int L) {
+  return num_passes(L) <= 1 ? 0 : tw_offset(L, num_passes(L) - 1) +
+      (1 << (ns_bits(L, num_passes(L) - 1) + pass_bits(L, num_passes(L) - 1)));
+}
+
+// ---------------------------------------------------------------------------
+// complex arithmetic
+// ---------------------------------------------------------------------------
+template <typename T> struct vec2;
+template <> struct vec2<double> { using type = double2; };
+template <> struct vec2<float> { using type = float2; };
+
+template <typename T>
+struct __align__(2 * sizeof(T)) cx {
+  T x, y;
+};
+
+template <typename T>
+__device__ __forceinline__ cx<T> cadd(cx<T> a, cx<T> b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T>
+__device__ __forceinline__ cx<T> csub(cx<T> a, cx<T> b) { return {a.x - b.x, a.y - b.y}; }
+// a * w
+template <typename T>
+__device__ __forceinline__ cx<T> cmul(cx<T> a, cx<T> w) {
+  return {fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x)};
+}
+// a * conj(w)
+template <typename T>
+__device__ __forceinline__ cx<T> cmulc(cx<T> a, cx<T> w) {
+  return {fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y)};
+}
+// multiply by the direction's twiddle: forward w, inverse conj(w)
+template <bool INV, typename T>
+__device__ __forceinline__ cx<T> ctw(cx<T> a, cx<T> w) {
+  if constexpr (INV) return cmulc(a, w); else return cmul(a, w);
+}
+
+template <typename T>
+__device__ __forceinline__ cx<T> ldg_cx(const cx<T>* p) {
+  auto v = __ldg(reinterpret_cast<const typename vec2<T>::type*>(p));
+  return {v.x, v.y};
+}
+
+// ---------------------------------------------------------------------------
+// small DFTs in registers: a[0..R-1] -> DFT_R(a), natural order
+// ---------------------------------------------------------------------------
+// exp(-2*pi*i*t/16) for the forward direction; INV conjugates.
+template <bool INV, typename T>
+__device__ __forceinline__ cx<T> mul_w16(cx<T> a, int t) {
+  const T c1 = T(0.923879532511286756128183189396788933);
+  const T s1 = T(0.382683432365089771728459984030398866);
+  const T h = T(0.707106781186547524400844362104849039);
+  // forward: w = cos - i sin; multiply a by w
+  T c, s;
+  switch (t & 15) {
+    case 0: return a;
+    case 4: return INV ? cx<T>{-a.y, a.x} : cx<T>{a.y, -a.x};
+    case 8: return {-a.x, -a.y};
+    case 12: return INV ? cx<T>{a.y, -a.x} : cx<T>{-a.y, a.x};
+    case 2: c = h; s = h; break;
+    case 6: c = -h; s = h; break;
+    case 10: c = -h; s = -h; break;
+    case 14: c = h; s = -h; break;
+    case 1: c = c1; s = s1; break;
+    case 3: c = s1; s = c1; break;
+    case 5: c = -s1; s = c1; break;
+    case 7: c = -c1; s = s1; break;
+    case 9: c = -c1; s = -s1; break;
+    case 11: c = -s1; s = -c1; break;
+    case 13: c = s1; s = -c1; break;
+    default: c = c1; s = -s1; break;  // 15
+  }
+  if (INV) s = -s;
+  // (a.x + i a.y)(c - i s)
+  return {fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s)};
+}
+
+template <int R, bool INV, typename T>
+struct DFT {
+  static __device__ __forceinline__ void run(cx<T>* a) {
+    constexpr int H = R / 2;
+    cx<T> e[H], o[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) { e[i] = a[2 * i]; o[i] = a[2 * i + 1]; }
+    DFT<H, INV, T>::run(e);
+    DFT<H, INV, T>::run(o);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      cx<T> t = mul_w16<INV>(o[k], k * (16 / R));
+      a[k] = cadd(e[k], t);
+      a[k + H] = csub(e[k], t);
+    }
+  }
+};
+template <bool INV, typename T>
+struct DFT<1, INV, T> {
+  static __device__ __forceinline__ void run(cx<T>*) {}
+};
+template <bool INV, typename T>
+struct DFT<2, INV, T> {
+  static __device__ __forceinline__ void run(cx<T>* a) {
+    cx<T> t = a[0];
+    a[0] = cadd(t, a[1]);
+    a[1] = csub(t, a[1]);
+  }
+};
+template <bool INV, typename T>
+struct DFT<4, INV, T> {
+  static __device__ __forceinline__ void run(cx<T>* a) {
+    cx<T> t0 = cadd(a[0], a[2]), t1 = csub(a[0], a[2]);
+    cx<T> t2 = cadd(a[1], a[3]), d = csub(a[1], a[3]);
+    // forward: -i*d ; inverse: +i*d
+    cx<T> t3 = INV ? cx<T>{-d.y, d.x} : cx<T>{d.y, -d.x};
+    a[0] = cadd(t0, t2);
+    a[2] = csub(t0, t2);
+    a[1] = cadd(t1, t3);
+    a[3] = csub(t1, t3);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stockham pass machinery
+// ---------------------------------------------------------------------------
+// SMEM index policy: element a of transform b lives at b*S + a + (a >> PS).
+template <int L>
+struct Shape {
+  static constexpr int N = 1 << L;
+  static constexpr int P = num_passes(L);
+  static constexpr int EB = ept_bits(L);
+  static constexpr int E = 1 << EB;
+  static constexpr int TPT = N / E;  // threads per transform
+  static constexpr int R0 = L == 0 ? 1 : (1 << pass_bits(L, 0));
+  static constexpr int RL = L == 0 ? 1 : (1 << pass_bits(L, P - 1));
+  static constexpr int TW = tw_total(L);
+  // element index held in v[u*R0+m] before pass 0 / in v[u*RL+m] after the last pass
+  static __device__ __forceinline__ int in_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / R0); }
+  static __device__ __forceinline__ int out_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / RL); }
+};
+
+template <typename T, int L, bool INV, int S, int PS>
+struct Stockham {
+  using SH = Shape<L>;
+  static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;
+
+  static __device__ __forceinline__ int sidx(int b, int a) { return b * S + a + (a >> PS); }
+
+  template <int p>
+  static __device__ __forceinline__ void compute(cx<T>* v, int tt, const cx<T>* __restrict__ tw) {
+    constexpr int R = 1 << pass_bits(L, p);
+    constexpr int NS = 1 << ns_bits(L, p);
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+      if constexpr (p > 0) {
+        const int j = tt + TPT * u;
+        const int k = j & (NS - 1);
+        const cx<T>* t = tw + tw_offset(L, p) + k * R;
+#pragma unroll
+        for (int m = 1; m < R; ++m) v[u * R + m] = ctw<INV>(v[u * R + m], ldg_cx(t + m));
+      }
+      DFT<R, INV, T>::run(v + u * R);
+    }
+  }
+
+  template <int p>
+  static __device__ __forceinline__ void store(cx<T>* sm, const cx<T>* v, int tt, int b) {
+    constexpr int R = 1 << pass_bits(L, p);
+    constexpr int NS = 1 << ns_bits(L, p);
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+      const int j = tt + TPT * u;
+      const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+      for (int m = 0; m < R; ++m) sm[sidx(b, base + m * NS)] = v[u * R + m];
+    }
+  }
+
+  template <int p>
+  static __device__ __forceinline__ void load(const cx<T>* sm, cx<T>* v, int tt, int b) {
+    constexpr int R = 1 << pass_bits(L, p);
+#pragma unroll
+    for (int u = 0; u < E / R; ++u) {
+      const int j = tt + TPT * u;
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[u * R + m] = sm[sidx(b, j + m * (N / R))];
+    }
+  }
+
+  template <int p>
+  static __device__ __forceinline__ void rest(cx<T>* sm, cx<T>* v, int tt, int b,
+                                              const cx<T>* __restrict__ tw) {
+    if constexpr (p < P) {
+      store<p - 1>(sm, v, tt, b);
+      __syncthreads();
+      load<p>(sm, v, tt, b);
+      __syncthreads();
+      compute<p>(v, tt, tw);
+      rest<p + 1>(sm, v, tt, b, tw);
+    }
+  }
+
+  // v holds pass-0 inputs (element in_elem(tt,u,m) in v[u*R0+m]); on return
+  // v[u*RL+m] holds output element out_elem(tt,u,m).  All threads of the CTA
+  // must call this (it synchronises when P > 1).
+  static __device__ __forceinline__ void run(cx<T>* sm, cx<T>* v, int tt, int b,
+                                             const cx<T>* __restrict__ tw) {
+    if constexpr (P > 0) {
+      compute<0>(v, tt, tw);
+      rest<1>(sm, v, tt, b, tw);
+    }
+  }
+
+  // write the final outputs into smem at their natural index (for the real
+  // transforms' post-processing that pairs bins k and N-k)
+  static __device__ __forceinline__ void store_natural(cx<T>* sm, const cx<T>* v, int tt, int b) {
+    constexpr int RL = SH::RL;
+#pragma unroll
+    for (int u = 0; u < E / RL; ++u)
+#pragma unroll
+      for (int m = 0; m < RL; ++m) sm[sidx(b, SH::out_elem(tt, u, m))] = v[u * RL + m];
+  }
+};
+
+}  // namespace tffft

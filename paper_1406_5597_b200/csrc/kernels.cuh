@@ -1,0 +1,283 @@
+// Stage kernels of the transpose-free slab 3D real FFT (sm_100a).
+//
+//  r2c_rows   stage 1a  : r2c along n2 of every row of the local planes
+//                         (reference kernels.py:203-209, 262-286 first half)
+//  col_fft    stage 1b  : c2c along n1 of every (plane, k) column, epilogue
+//                         routes peer bands to the exchange staging buffer
+//             stage 3   : c2c along n0 of every STRIDED_INPLACE column, read
+//                         in place through the two-level stride
+//                         (kernels.py:176-200, layout.py:201-219)
+//             stage 3'/1b' likewise for the inverse
+//  c2r_rows   stage 1a' : c2r along n2, 1/(n0 n1 n2) folded in, Hermitian
+//                         consistency statistics (kernels.py:212-239)
+#pragma once
+#include "fft_engine.cuh"
+
+namespace tffft {
+
+// Column c of a batch: base = (c / cpb) * grp_stride + (c % cpb).
+// Element e of a column: (e & (1<<ic_shift)-1) * inner_stride + (e >> ic_shift) * block_stride.
+// Redirect (peer bands): band = e >> band_shift; if staging && band != self_band
+//   -> staging + band*stg_band + (e & band_mask)*stg_within + (c / cpb)*stg_grp + (c % cpb)
+struct ColParams {
+  void* data;
+  void* staging;
+  const void* tw;
+  long long ncols;
+  int cpb;
+  long long grp_stride;
+  int ic_shift;
+  long long inner_stride, block_stride;
+  int band_shift, self_band;
+  long long stg_band, stg_within, stg_grp;
+};
+
+// Rows: row r of real data at real + r*n2 (reals); complex row at spec + r*n2c.
+struct RowParams {
+  void* real;
+  void* spec;
+  const void* tw;       // pass tables for N = n2/2
+  const void* tw_post;  // exp(-2 pi i k / n2), k < n2/2
+  long long nrows;
+  int n2c;
+  int rows_per_plane;
+  double scale;                   // c2r output scale
+  unsigned long long* stats;      // c2r: per plane [m2, edge, residue] as ordered doubles
+};
+
+template <int L> struct ColCfg {
+  static constexpr int TPT = Shape<L>::TPT;
+  static constexpr int B = L >= 12 ? 2 : (256 / TPT > 4 ? 256 / TPT : 4);
+  static constexpr int THREADS = TPT * B;
+  static constexpr int S = Shape<L>::N + 1;  // odd row stride: 8 adjacent columns hit 8 bank groups
+  static constexpr int PS = 30;              // no in-row padding
+  static constexpr bool SMEM = Shape<L>::P > 1;
+};
+
+template <int L> struct RowCfg {
+  static constexpr int TPT = Shape<L>::TPT;
+  static constexpr int B = 256 / TPT > 1 ? 256 / TPT : 1;
+  static constexpr int THREADS = TPT * B;
+  static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;  // one pad slot per E elements
+  static constexpr int N = Shape<L>::N;
+  static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
+};
+
+template <typename T, int L>
+__host__ __device__ constexpr size_t col_smem_bytes() {
+  return ColCfg<L>::SMEM ? sizeof(cx<T>) * ColCfg<L>::B * ColCfg<L>::S : 0;
+}
+template <typename T, int L>
+__host__ __device__ constexpr size_t row_smem_bytes() {
+  return sizeof(cx<T>) * RowCfg<L>::B * RowCfg<L>::S;
+}
+
+// ---------------------------------------------------------------------------
+// batched column c2c (stages 1b, 3, 3', 1b')
+// ---------------------------------------------------------------------------
+template <typename T, int L, bool INV>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+col_fft_kernel(const ColParams prm) {
+  using CF = ColCfg<L>;
+  using SH = Shape<L>;
+  using ST = Stockham<T, L, INV, CF::S, CF::PS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+  const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
+  cx<T>* data = reinterpret_cast<cx<T>*>(prm.data);
+
+  const int b = threadIdx.x % CF::B;
+  const int tt = threadIdx.x / CF::B;
+  const long long c = (long long)blockIdx.x * CF::B + b;
+  const bool valid = c < prm.ncols;
+  const unsigned cq = valid ? (unsigned)(c / prm.cpb) : 0u;
+  const unsigned cr = valid ? (unsigned)(c - (long long)cq * prm.cpb) : 0u;
+  const long long base = (long long)cq * prm.grp_stride + cr;
+  const int icm = (1 << prm.ic_shift) - 1;
+
+  cx<T> v[SH::E];
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::R0; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::R0; ++m) {
+      const int e = SH::in_elem(tt, u, m);
+      const long long off = base + (long long)(e & icm) * prm.inner_stride +
+                            (long long)(e >> prm.ic_shift) * prm.block_stride;
+      v[u * SH::R0 + m] = valid ? data[off] : cx<T>{T(0), T(0)};
+    }
+
+  ST::run(sm, v, tt, b, tw);
+
+  if (!valid) return;
+  cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging);
+  const int bmask = (1 << prm.band_shift) - 1;
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::RL; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::RL; ++m) {
+      const int e = SH::out_elem(tt, u, m);
+      const int band = e >> prm.band_shift;
+      if (stg != nullptr && band != prm.self_band) {
+        const long long off = (long long)band * prm.stg_band + (long long)(e & bmask) * prm.stg_within +
+                              (long long)cq * prm.stg_grp + cr;
+        stg[off] = v[u * SH::RL + m];
+      } else {
+        const long long off = base + (long long)(e & icm) * prm.inner_stride +
+                              (long long)(e >> prm.ic_shift) * prm.block_stride;
+        data[off] = v[u * SH::RL + m];
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// r2c along n2 (packed: n2 reals -> N = n2/2 complex FFT -> n2/2+1 bins)
+// ---------------------------------------------------------------------------
+template <typename T, int L>
+__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+r2c_rows_kernel(const RowParams prm) {
+  using RC = RowCfg<L>;
+  using SH = Shape<L>;
+  using ST = Stockham<T, L, false, RC::S, RC::PS>;
+  constexpr int N = SH::N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+  const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
+  const cx<T>* twp = reinterpret_cast<const cx<T>*>(prm.tw_post);
+
+  const int tt = threadIdx.x % SH::TPT;
+  const int b = threadIdx.x / SH::TPT;
+  const long long row = (long long)blockIdx.x * RC::B + b;
+  const bool valid = row < prm.nrows;
+  const cx<T>* in = reinterpret_cast<const cx<T>*>(reinterpret_cast<const T*>(prm.real) + (valid ? row : 0) * (2LL * N));
+
+  cx<T> v[SH::E];
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::R0; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::R0; ++m) v[u * SH::R0 + m] = in[SH::in_elem(tt, u, m)];
+
+  ST::run(sm, v, tt, b, tw);
+  if constexpr (SH::P > 1) __syncthreads();  // last exchange reads done before reuse
+  ST::store_natural(sm, v, tt, b);
+  __syncthreads();
+  if (!valid) return;
+
+  cx<T>* out = reinterpret_cast<cx<T>*>(prm.spec) + row * prm.n2c;
+  const T half = T(0.5);
+#pragma unroll
+  for (int q = 0; q < SH::E; ++q) {
+    const int k = tt + SH::TPT * q;
+    cx<T> X;
+    if (k == 0) {
+      const cx<T> z0 = sm[ST::sidx(b, 0)];
+      X = {z0.x + z0.y, T(0)};
+      out[N] = cx<T>{z0.x - z0.y, T(0)};
+    } else {
+      const cx<T> A = sm[ST::sidx(b, k)];
+      const cx<T> Bz = sm[ST::sidx(b, N - k)];
+      const cx<T> S = {A.x + Bz.x, A.y - Bz.y};   // A + conj(B)
+      const cx<T> D = {A.x - Bz.x, A.y + Bz.y};   // A - conj(B)
+      const cx<T> Tt = cmul(D, ldg_cx(twp + k));
+      X = {half * (S.x + Tt.y), half * (S.y - Tt.x)};
+    }
+    out[k] = X;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// c2r along n2 (packed inverse), scale folded in, consistency statistics
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ord(double x) { return __double_as_longlong(x); }
+
+template <typename T, int L>
+__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+c2r_rows_kernel(const RowParams prm) {
+  using RC = RowCfg<L>;
+  using SH = Shape<L>;
+  using ST = Stockham<T, L, true, RC::S, RC::PS>;
+  constexpr int N = SH::N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+  const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
+  const cx<T>* twp = reinterpret_cast<const cx<T>*>(prm.tw_post);
+
+  const int tt = threadIdx.x % SH::TPT;
+  const int b = threadIdx.x / SH::TPT;
+  const long long row = (long long)blockIdx.x * RC::B + b;
+  const bool valid = row < prm.nrows;
+  const cx<T>* in = reinterpret_cast<const cx<T>*>(prm.spec) + (valid ? row : 0) * prm.n2c;
+
+  double m2 = 0.0, edge = 0.0, resid = 0.0;
+#pragma unroll
+  for (int q = 0; q <= SH::E; ++q) {
+    const int k = tt + SH::TPT * q;
+    if (k <= N && (q < SH::E || tt == 0)) {
+      cx<T> X = valid ? in[k] : cx<T>{T(0), T(0)};
+      const double a2 = (double)X.x * X.x + (double)X.y * X.y;
+      m2 = fmax(m2, a2);
+      if (k == 0 || k == N) {
+        const double im = fabs((double)X.y);
+        edge = fmax(edge, im);
+        resid += im;
+        X.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
+      }
+      sm[ST::sidx(b, k)] = X;
+    }
+  }
+  // statistics: reduce over the TPT threads of this row, one atomic per row-warp
+  constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) {
+    m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o, W));
+    edge = fmax(edge, __shfl_xor_sync(0xffffffffu, edge, o, W));
+    resid += __shfl_xor_sync(0xffffffffu, resid, o, W);
+  }
+  if (valid && prm.stats != nullptr && (tt % W) == 0) {
+    unsigned long long* st = prm.stats + 3 * (row / prm.rows_per_plane);
+    atomicMax(st + 0, ord(m2));
+    if (tt == 0) {
+      atomicMax(st + 1, ord(edge));
+      atomicMax(st + 2, ord(resid));
+    }
+  }
+  __syncthreads();
+
+  cx<T> v[SH::E];
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::R0; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::R0; ++m) {
+      const int k = SH::in_elem(tt, u, m);
+      const cx<T> A = sm[ST::sidx(b, k)];
+      const cx<T> Bx = sm[ST::sidx(b, N - k)];
+      const cx<T> S = {A.x + Bx.x, A.y - Bx.y};  // A + conj(B)
+      const cx<T> D = {A.x - Bx.x, A.y + Bx.y};  // A - conj(B)
+      const cx<T> Tt = cmulc(D, ldg_cx(twp + k)); // exp(+2 pi i k / n2) * D
+      v[u * SH::R0 + m] = {S.x - Tt.y, S.y + Tt.x};
+    }
+  __syncthreads();
+
+  ST::run(sm, v, tt, b, tw);
+  if (!valid) return;
+
+  T* out = reinterpret_cast<T*>(prm.real) + row * (2LL * N);
+  cx<T>* outc = reinterpret_cast<cx<T>*>(out);
+  const T s = T(prm.scale);
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::RL; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::RL; ++m) {
+      const cx<T> z = v[u * SH::RL + m];
+      outc[SH::out_elem(tt, u, m)] = cx<T>{z.x * s, z.y * s};
+    }
+}
+
+// host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)
+template <typename T>
+cudaError_t launch_col_fft(int L, bool inv, const ColParams& p, cudaStream_t s);
+template <typename T>
+cudaError_t launch_r2c_rows(int L, const RowParams& p, cudaStream_t s);
+template <typename T>
+cudaError_t launch_c2r_rows(int L, const RowParams& p, cudaStream_t s);
+
+}  // namespace tffft

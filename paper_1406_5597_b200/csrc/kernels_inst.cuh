@@ -1,0 +1,89 @@
+// Explicit instantiation + runtime dispatch of the stage kernels for one
+// precision.  Included by kernels_f64.cu / kernels_f32.cu with TFFFT_REAL set.
+#include "kernels.cuh"
+
+namespace tffft {
+
+template <typename K>
+static cudaError_t prep_smem(K kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <typename T, int L, bool INV>
+static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
+  using CF = ColCfg<L>;
+  const size_t sm = col_smem_bytes<T, L>();
+  auto k = col_fft_kernel<T, L, INV>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  const long long blocks = (p.ncols + CF::B - 1) / CF::B;
+  if (blocks <= 0) return cudaSuccess;
+  k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int L>
+static cudaError_t r2c_one(const RowParams& p, cudaStream_t s) {
+  using RC = RowCfg<L>;
+  const size_t sm = row_smem_bytes<T, L>();
+  auto k = r2c_rows_kernel<T, L>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  const long long blocks = (p.nrows + RC::B - 1) / RC::B;
+  if (blocks <= 0) return cudaSuccess;
+  k<<<(unsigned)blocks, RC::THREADS, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int L>
+static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
+  using RC = RowCfg<L>;
+  const size_t sm = row_smem_bytes<T, L>();
+  auto k = c2r_rows_kernel<T, L>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  const long long blocks = (p.nrows + RC::B - 1) / RC::B;
+  if (blocks <= 0) return cudaSuccess;
+  k<<<(unsigned)blocks, RC::THREADS, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+#define TFFFT_COL_CASE(LL) \
+  case LL: return inv ? col_one<TFFFT_REAL, LL, true>(p, s) : col_one<TFFFT_REAL, LL, false>(p, s);
+#define TFFFT_ROW_CASE(LL, FN) \
+  case LL: return FN<TFFFT_REAL, LL>(p, s);
+
+template <>
+cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, const ColParams& p, cudaStream_t s) {
+  switch (L) {
+    TFFFT_COL_CASE(1) TFFFT_COL_CASE(2) TFFFT_COL_CASE(3) TFFFT_COL_CASE(4)
+    TFFFT_COL_CASE(5) TFFFT_COL_CASE(6) TFFFT_COL_CASE(7) TFFFT_COL_CASE(8)
+    TFFFT_COL_CASE(9) TFFFT_COL_CASE(10) TFFFT_COL_CASE(11) TFFFT_COL_CASE(12)
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <>
+cudaError_t launch_r2c_rows<TFFFT_REAL>(int L, const RowParams& p, cudaStream_t s) {
+  switch (L) {
+    TFFFT_ROW_CASE(0, r2c_one) TFFFT_ROW_CASE(1, r2c_one) TFFFT_ROW_CASE(2, r2c_one)
+    TFFFT_ROW_CASE(3, r2c_one) TFFFT_ROW_CASE(4, r2c_one) TFFFT_ROW_CASE(5, r2c_one)
+    TFFFT_ROW_CASE(6, r2c_one) TFFFT_ROW_CASE(7, r2c_one) TFFFT_ROW_CASE(8, r2c_one)
+    TFFFT_ROW_CASE(9, r2c_one) TFFFT_ROW_CASE(10, r2c_one) TFFFT_ROW_CASE(11, r2c_one)
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <>
+cudaError_t launch_c2r_rows<TFFFT_REAL>(int L, const RowParams& p, cudaStream_t s) {
+  switch (L) {
+    TFFFT_ROW_CASE(0, c2r_one) TFFFT_ROW_CASE(1, c2r_one) TFFFT_ROW_CASE(2, c2r_one)
+    TFFFT_ROW_CASE(3, c2r_one) TFFFT_ROW_CASE(4, c2r_one) TFFFT_ROW_CASE(5, c2r_one)
+    TFFFT_ROW_CASE(6, c2r_one) TFFFT_ROW_CASE(7, c2r_one) TFFFT_ROW_CASE(8, c2r_one)
+    TFFFT_ROW_CASE(9, c2r_one) TFFFT_ROW_CASE(10, c2r_one) TFFFT_ROW_CASE(11, c2r_one)
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tffft

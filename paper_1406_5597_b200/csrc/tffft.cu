@@ -1,0 +1,796 @@
+// Host runtime of the transpose-free slab 3D real FFT: plans, twiddle tables,
+// the two exchange transports (NCCL over NVLink; in-process local fabric on
+// one device) and the forward / inverse stage orchestration behind the C ABI
+// declared in include/tffft.h.
+//
+// Pipeline (reference dfft.py:148-215, STRIDED strategy):
+//   forward: r2c rows (n2) -> c2c columns (n1), epilogue splits self band /
+//            peer bands -> exchange (peer chunks land in the vacated bands,
+//            exchange.py:263-276) -> in-place c2c along n0 over the
+//            STRIDED_INPLACE columns (kernels.py:176-200)
+//   inverse: c2c along n0 (epilogue splits peer blocks) -> exchange ->
+//            c2c columns (n1) -> c2r rows (n2) with 1/(n0 n1 n2).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tffft.h"
+#include "kernels.cuh"
+#include "nccl.h"
+
+using namespace tffft;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail(TFFFT_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define TRY(expr)               \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != TFFFT_OK) return _s; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily so the library loads (and its symbols can be checked)
+// on machines without a GPU or without NCCL.
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  bool loaded = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("TFFFT_NCCL_LIBRARY");
+    void* h = nullptr;
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // torch's copy
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.err = dlerror() ? dlerror() : "libnccl.so.2 not found";
+      return;
+    }
+#define LOAD(name)                                                           \
+  api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name));   \
+  if (!api.name) { api.err = "missing symbol nccl" #name; return; }
+    LOAD(GetUniqueId) LOAD(CommInitRank) LOAD(CommDestroy) LOAD(CommAbort) LOAD(CommGetAsyncError)
+    LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd) LOAD(GetErrorString)
+#undef LOAD
+    api.loaded = true;
+  });
+  return api;
+}
+
+#define NCCL_TRY(expr)                                                                   \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess)                                                               \
+      return fail(TFFFT_ERR_TRANSPORT, "%s failed: %s", #expr, nccl().GetErrorString(_r)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// local fabric: p ranks in one process on one device (transport.py:188-302)
+// ---------------------------------------------------------------------------
+struct LocalFabric {
+  int p;
+  int device;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  bool aborted = false;
+  double timeout_s = 600.0;
+  // per plan sequence number: each rank's staging pointer and events
+  struct Slot {
+    std::vector<void*> staging;
+    std::vector<cudaEvent_t> ready, done;
+  };
+  std::vector<Slot> slots;
+  std::atomic<int> refs{0};
+
+  explicit LocalFabric(int p_, int dev) : p(p_), device(dev) {}
+
+  // generation barrier with abort and timeout (transport.py:225-233, 290-302)
+  int barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return fail(TFFFT_ERR_TRANSPORT, "fabric aborted");
+    uint64_t gen = generation;
+    if (++arrived == p) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return TFFFT_OK;
+    }
+    bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
+                          [&] { return generation != gen || aborted; });
+    if (aborted) return fail(TFFFT_ERR_TRANSPORT, "fabric aborted while waiting at barrier");
+    if (!ok) {
+      aborted = true;
+      cv.notify_all();
+      return fail(TFFFT_ERR_TRANSPORT, "barrier timed out after %.0f s (a rank did not arrive)", timeout_s);
+    }
+    return TFFFT_OK;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+  Slot& slot(int seq) {
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)slots.size() <= seq) slots.resize(seq + 1);
+    Slot& s = slots[seq];
+    if ((int)s.staging.size() != p) {
+      s.staging.assign(p, nullptr);
+      s.ready.assign(p, nullptr);
+      s.done.assign(p, nullptr);
+    }
+    return s;
+  }
+};
+
+struct tffft_comm_s {
+  int p = 1, rank = 0, device = 0;
+  bool is_nccl = false;
+  ncclComm_t nccl = nullptr;
+  std::shared_ptr<LocalFabric> fabric;
+  int plan_seq = 0;
+};
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+struct StageEvents {
+  cudaEvent_t e[4];
+  bool forward;
+};
+
+struct tffft_plan_s {
+  tffft_comm_t comm = nullptr;
+  int n0 = 0, n1 = 0, n2 = 0, p = 1, rank = 0, dtype = TFFFT_F64, pattern = TFFFT_PAIRWISE;
+  int L0 = 0, L1 = 0, L2h = 0;
+  int n0p = 0, n1p = 0, n2c = 0;
+  size_t esz = 16;  // complex element bytes
+  int seq = 0;
+  void* staging = nullptr;
+  void* tw0 = nullptr;
+  void* tw1 = nullptr;
+  void* tw2 = nullptr;
+  void* tw2post = nullptr;
+  unsigned long long* stats = nullptr;
+  void** pull_ptrs = nullptr;  // local fabric: device array [2 * nchunks] of (src, dst)
+  size_t workspace = 0;
+  bool timing = false;
+  std::vector<StageEvents> events;
+  uint64_t counters[3] = {0, 0, 0};
+  uint64_t launches = 0;
+  cudaStream_t last_inverse_stream = nullptr;
+  bool inverse_ran = false;
+};
+
+static bool pow2(long long n) { return n >= 1 && (n & (n - 1)) == 0; }
+static int ilog2(long long n) { int l = 0; while ((1LL << l) < n) ++l; return l; }
+
+// pass twiddle tables for length 2^L (see fft_engine.cuh): block for pass p>=1
+// holds exp(-2 pi i m k / (Ns R)) at [k*R + m]
+static std::vector<double> pass_table(int L) {
+  std::vector<double> t;
+  const int P = num_passes(L);
+  t.assign(2 * (size_t)std::max(tw_total(L), 1), 0.0);
+  for (int p = 1; p < P; ++p) {
+    const long long R = 1LL << pass_bits(L, p), NS = 1LL << ns_bits(L, p), M = NS * R;
+    const size_t off = tw_offset(L, p);
+    for (long long k = 0; k < NS; ++k)
+      for (long long m = 0; m < R; ++m) {
+        const long double a = -2.0L * 3.141592653589793238462643383279502884L *
+                              (long double)((m * k) % M) / (long double)M;
+        t[2 * (off + k * R + m)] = (double)cosl(a);
+        t[2 * (off + k * R + m) + 1] = (double)sinl(a);
+      }
+  }
+  return t;
+}
+
+// exp(-2 pi i k / n) for k < n/2 (reference twiddle convention, kernels.py:76-81)
+static std::vector<double> post_table(int n) {
+  std::vector<double> t(2 * (size_t)std::max(n / 2, 1), 0.0);
+  for (int k = 0; k < n / 2; ++k) {
+    const long double a = -2.0L * 3.141592653589793238462643383279502884L * k / (long double)n;
+    t[2 * k] = (double)cosl(a);
+    t[2 * k + 1] = (double)sinl(a);
+  }
+  return t;
+}
+
+static int upload_table(const std::vector<double>& t, int dtype, void** dev, size_t* bytes) {
+  const size_t n = t.size();
+  if (dtype == TFFFT_F64) {
+    CUDA_TRY(cudaMalloc(dev, n * sizeof(double)));
+    CUDA_TRY(cudaMemcpy(*dev, t.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    *bytes += n * sizeof(double);
+  } else {
+    std::vector<float> f(n);
+    for (size_t i = 0; i < n; ++i) f[i] = (float)t[i];
+    CUDA_TRY(cudaMalloc(dev, n * sizeof(float)));
+    CUDA_TRY(cudaMemcpy(*dev, f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+    *bytes += n * sizeof(float);
+  }
+  return TFFFT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel launch helpers
+// ---------------------------------------------------------------------------
+static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, const ColParams& prm, cudaStream_t s) {
+  pl->launches++;
+  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, prm, s)
+                                : launch_col_fft<float>(L, inv, prm, s);
+}
+static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
+  pl->launches++;
+  return pl->dtype == TFFFT_F64 ? launch_r2c_rows<double>(pl->L2h, prm, s)
+                                : launch_r2c_rows<float>(pl->L2h, prm, s);
+}
+static cudaError_t c2r_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
+  pl->launches++;
+  return pl->dtype == TFFFT_F64 ? launch_c2r_rows<double>(pl->L2h, prm, s)
+                                : launch_c2r_rows<float>(pl->L2h, prm, s);
+}
+
+// local-fabric pull: chunk c copies `words` W-sized words from ptrs[2c] to ptrs[2c+1]
+template <typename W>
+__global__ void pull_chunks_kernel(void* const* __restrict__ ptrs, long long words, int nchunks) {
+  const int c = blockIdx.y;
+  if (c >= nchunks) return;
+  const W* __restrict__ src = reinterpret_cast<const W*>(ptrs[2 * c]);
+  W* __restrict__ dst = reinterpret_cast<W*>(ptrs[2 * c + 1]);
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (long long)gridDim.x * blockDim.x)
+    dst[w] = src[w];
+}
+
+// ---------------------------------------------------------------------------
+// stage launchers
+// ---------------------------------------------------------------------------
+// stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of the local slab
+static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  ColParams c{};
+  c.data = spec;
+  c.tw = pl->tw1;
+  c.ncols = (long long)pl->n0p * pl->n2c;
+  c.cpb = pl->n2c;
+  c.grp_stride = (long long)pl->n1 * pl->n2c;
+  c.ic_shift = 30;
+  c.inner_stride = pl->n2c;
+  c.block_stride = 0;
+  c.band_shift = ilog2(pl->n1p);
+  c.self_band = pl->rank;
+  c.staging = nullptr;
+  if (!inv && pl->p > 1) {
+    // forward epilogue: band q != rank -> staging[q][i][j][k]
+    c.staging = pl->staging;
+    c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
+    c.stg_within = pl->n2c;
+    c.stg_grp = (long long)pl->n1p * pl->n2c;
+  }
+  CUDA_TRY(col_launch(pl, pl->L1, inv, c, s));
+  return TFFFT_OK;
+}
+
+// stage 3 / 3': c2c along n0 of every STRIDED_INPLACE column c = j*n2c + k
+static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  ColParams c{};
+  c.data = spec;
+  c.tw = pl->tw0;
+  c.ncols = (long long)pl->n1p * pl->n2c;
+  c.cpb = (int)std::min<long long>(c.ncols, 1LL << 30);
+  c.grp_stride = 0;
+  c.ic_shift = ilog2(pl->n0p);
+  c.inner_stride = (long long)pl->n1 * pl->n2c;
+  c.block_stride = (long long)pl->n1p * pl->n2c;
+  c.band_shift = ilog2(pl->n0p);
+  c.self_band = pl->rank;
+  c.staging = nullptr;
+  if (inv && pl->p > 1) {
+    // inverse epilogue: block s != rank -> staging[s][i][c]
+    c.staging = pl->staging;
+    c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
+    c.stg_within = (long long)pl->n1p * pl->n2c;
+    c.stg_grp = 0;
+  }
+  CUDA_TRY(col_launch(pl, pl->L0, inv, c, s));
+  return TFFFT_OK;
+}
+
+static RowParams row_params(tffft_plan_t pl, void* real, void* spec) {
+  RowParams r{};
+  r.real = real;
+  r.spec = spec;
+  r.tw = pl->tw2;
+  r.tw_post = pl->tw2post;
+  r.nrows = (long long)pl->n0p * pl->n1;
+  r.n2c = pl->n2c;
+  r.rows_per_plane = pl->n1;
+  r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
+  r.stats = pl->stats;
+  return r;
+}
+
+static uint64_t wire_bytes(tffft_plan_t pl) {
+  return (uint64_t)(pl->p - 1) * pl->n0p * pl->n1p * pl->n2c * pl->esz;
+}
+
+// all peers must have finished pulling from my staging before I overwrite it
+static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
+  if (pl->p == 1 || pl->comm->is_nccl) return TFFFT_OK;
+  auto& slot = pl->comm->fabric->slot(pl->seq);
+  for (int q = 0; q < pl->p; ++q)
+    if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.done[q], 0));
+  return TFFFT_OK;
+}
+
+// the exchange proper: staging[q][i] -> peer q's spectral slab at band rank of plane i
+static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  if (pl->p == 1) return TFFFT_OK;
+  const long long chunk = (long long)pl->n1p * pl->n2c;  // complex elements
+  if (pl->comm->is_nccl) {
+    NcclApi& api = nccl();
+    const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
+    char* stg = static_cast<char*>(pl->staging);
+    char* dst = static_cast<char*>(spec);
+    NCCL_TRY(api.GroupStart());
+    for (int d = 1; d < pl->p; ++d) {
+      const int to = (pl->rank + d) % pl->p, from = (pl->rank - d + pl->p) % pl->p;
+      for (int i = 0; i < pl->n0p; ++i) {
+        NCCL_TRY(api.Send(stg + ((long long)to * pl->n0p + i) * chunk * pl->esz, 2 * chunk, dt, to,
+                          pl->comm->nccl, s));
+        NCCL_TRY(api.Recv(dst + ((long long)i * pl->n1 * pl->n2c + (long long)from * chunk) * pl->esz,
+                          2 * chunk, dt, from, pl->comm->nccl, s));
+      }
+    }
+    NCCL_TRY(api.GroupEnd());
+  } else {
+    LocalFabric& fab = *pl->comm->fabric;
+    auto& slot = fab.slot(pl->seq);
+    CUDA_TRY(cudaEventRecord(slot.ready[pl->rank], s));
+    TRY(fab.barrier());
+    for (int q = 0; q < pl->p; ++q)
+      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.ready[q], 0));
+    // 16-byte words when every chunk (and so every chunk offset) is a multiple of 16 bytes
+    const long long bytes = chunk * (long long)pl->esz;
+    const bool wide = bytes % 16 == 0 && reinterpret_cast<uintptr_t>(spec) % 16 == 0;
+    const long long words = wide ? bytes / 16 : bytes / 8;
+    const int nchunks = (pl->p - 1) * pl->n0p;
+    dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 64), (unsigned)nchunks);
+    if (wide)
+      pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(pl->pull_ptrs, words, nchunks);
+    else
+      pull_chunks_kernel<int2><<<grid, 256, 0, s>>>(pl->pull_ptrs, words, nchunks);
+    pl->launches++;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(slot.done[pl->rank], s));
+    TRY(fab.barrier());
+  }
+  pl->counters[1] += wire_bytes(pl);
+  return TFFFT_OK;
+}
+
+// build the pull pointer list once all ranks registered their staging buffers
+static int fabric_setup(tffft_plan_t pl, void* /*unused*/) {
+  LocalFabric& fab = *pl->comm->fabric;
+  auto& slot = fab.slot(pl->seq);
+  slot.staging[pl->rank] = pl->staging;
+  CUDA_TRY(cudaEventCreateWithFlags(&slot.ready[pl->rank], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&slot.done[pl->rank], cudaEventDisableTiming));
+  TRY(fab.barrier());
+  return TFFFT_OK;
+}
+
+// the pull list depends on the destination spectral buffer: (re)built per call
+static int fabric_pull_list(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  LocalFabric& fab = *pl->comm->fabric;
+  auto& slot = fab.slot(pl->seq);
+  const long long chunk = (long long)pl->n1p * pl->n2c;
+  std::vector<void*> h;
+  h.reserve(2 * (size_t)(pl->p - 1) * pl->n0p);
+  for (int q = 0; q < pl->p; ++q) {
+    if (q == pl->rank) continue;
+    char* src = static_cast<char*>(slot.staging[q]);
+    for (int i = 0; i < pl->n0p; ++i) {
+      h.push_back(src + ((long long)pl->rank * pl->n0p + i) * chunk * pl->esz);
+      h.push_back(static_cast<char*>(spec) + ((long long)i * pl->n1 * pl->n2c + (long long)q * chunk) * pl->esz);
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(pl->pull_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+  // the pageable copy above is synchronous w.r.t. the host buffer, so h may go out of scope
+  return TFFFT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+#pragma GCC visibility push(default)
+
+const char* tffft_last_error(void) { return g_last_error.c_str(); }
+int tffft_version(void) { return 100; }
+
+int tffft_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(TFFFT_ERR_CONFIGURATION, "null output");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(TFFFT_ERR_TRANSPORT, "NCCL unavailable: %s", api.err.c_str());
+  ncclUniqueId id;
+  NCCL_TRY(api.GetUniqueId(&id));
+  memcpy(out, id.internal, 128);
+  return TFFFT_OK;
+}
+
+int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tffft_comm_t* comm) {
+  if (!comm || !id) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (p < 1 || rank < 0 || rank >= p) return fail(TFFFT_ERR_CONFIGURATION, "rank %d outside [0, %d)", rank, p);
+  auto c = std::make_unique<tffft_comm_s>();
+  c->p = p;
+  c->rank = rank;
+  c->device = device;
+  c->is_nccl = true;
+  CUDA_TRY(cudaSetDevice(device));
+  if (p > 1) {
+    NcclApi& api = nccl();
+    if (!api.loaded) return fail(TFFFT_ERR_TRANSPORT, "NCCL unavailable: %s", api.err.c_str());
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, 128);
+    NCCL_TRY(api.CommInitRank(&c->nccl, p, uid, rank));
+  }
+  *comm = c.release();
+  return TFFFT_OK;
+}
+
+int tffft_comm_init_local(int p, int device, tffft_comm_t* comms) {
+  if (!comms) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (p < 1) return fail(TFFFT_ERR_CONFIGURATION, "communicator group needs p >= 1, got %d", p);
+  auto fab = std::make_shared<LocalFabric>(p, device);
+  const char* to = getenv("TFFFT_FABRIC_TIMEOUT");
+  if (to) fab->timeout_s = atof(to);
+  for (int r = 0; r < p; ++r) {
+    auto* c = new tffft_comm_s();
+    c->p = p;
+    c->rank = r;
+    c->device = device;
+    c->fabric = fab;
+    comms[r] = c;
+  }
+  return TFFFT_OK;
+}
+
+int tffft_comm_rank(tffft_comm_t c, int* r) {
+  if (!c || !r) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *r = c->rank;
+  return TFFFT_OK;
+}
+int tffft_comm_size(tffft_comm_t c, int* p) {
+  if (!c || !p) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *p = c->p;
+  return TFFFT_OK;
+}
+int tffft_comm_device(tffft_comm_t c, int* d) {
+  if (!c || !d) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *d = c->device;
+  return TFFFT_OK;
+}
+
+int tffft_comm_abort(tffft_comm_t c) {
+  if (!c) return fail(TFFFT_ERR_CONFIGURATION, "null comm");
+  if (c->fabric) c->fabric->abort();
+  if (c->nccl) {
+    NCCL_TRY(nccl().CommAbort(c->nccl));
+    c->nccl = nullptr;
+  }
+  return TFFFT_OK;
+}
+
+int tffft_comm_destroy(tffft_comm_t c) {
+  if (!c) return TFFFT_OK;
+  if (c->nccl) nccl().CommDestroy(c->nccl);
+  delete c;
+  return TFFFT_OK;
+}
+
+int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm_t comm, tffft_plan_t* out) {
+  if (!comm || !out) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  const int p = comm->p;
+  // layout.py:63-66 (powers of two), layout.py:83-93 (validate)
+  const int ns[3] = {n0, n1, n2};
+  const char* nm[3] = {"n0", "n1", "n2"};
+  for (int a = 0; a < 3; ++a) {
+    if (!pow2(ns[a])) return fail(TFFFT_ERR_CONFIGURATION, "%s must be a positive power of two, got %d", nm[a], ns[a]);
+    if (ns[a] < 2) return fail(TFFFT_ERR_CONFIGURATION, "%s must be a power of two >= 2, got %d", nm[a], ns[a]);
+    if (ns[a] > (1 << kMaxLog)) return fail(TFFFT_ERR_SIZE, "%s=%d exceeds the supported maximum %d", nm[a], ns[a], 1 << kMaxLog);
+  }
+  if (n0 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n0 (%d does not divide %d)", p, n0);
+  if (n1 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n1 (%d does not divide %d)", p, n1);
+  if (dtype != TFFFT_F64 && dtype != TFFFT_F32) return fail(TFFFT_ERR_CONFIGURATION, "unknown dtype %d", dtype);
+  if (pattern != TFFFT_PAIRWISE)
+    return fail(TFFFT_ERR_CONFIGURATION, "only the PAIRWISE comm pattern is implemented on the GPU");
+
+  auto pl = std::make_unique<tffft_plan_s>();
+  pl->comm = comm;
+  pl->n0 = n0; pl->n1 = n1; pl->n2 = n2;
+  pl->p = p; pl->rank = comm->rank; pl->dtype = dtype; pl->pattern = pattern;
+  pl->L0 = ilog2(n0); pl->L1 = ilog2(n1); pl->L2h = ilog2(n2) - 1;
+  pl->n0p = n0 / p; pl->n1p = n1 / p; pl->n2c = n2 / 2 + 1;
+  pl->esz = dtype == TFFFT_F64 ? 16 : 8;
+  CUDA_TRY(cudaSetDevice(comm->device));
+
+  size_t ws = 0;
+  TRY(upload_table(pass_table(pl->L0), dtype, &pl->tw0, &ws));
+  TRY(upload_table(pass_table(pl->L1), dtype, &pl->tw1, &ws));
+  TRY(upload_table(pass_table(pl->L2h), dtype, &pl->tw2, &ws));
+  TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
+  CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
+  CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
+  ws += sizeof(unsigned long long) * 3 * pl->n0p;
+  if (p > 1) {
+    const size_t sb = (size_t)p * pl->n0p * pl->n1p * pl->n2c * pl->esz;
+    CUDA_TRY(cudaMalloc(&pl->staging, sb));
+    ws += sb;
+    if (!comm->is_nccl) {
+      const size_t nptr = 2 * (size_t)(p - 1) * pl->n0p;
+      CUDA_TRY(cudaMalloc(&pl->pull_ptrs, nptr * sizeof(void*)));
+      ws += nptr * sizeof(void*);
+      pl->seq = comm->plan_seq++;
+      TRY(fabric_setup(pl.get(), nullptr));
+    }
+  }
+  pl->workspace = ws;
+  *out = pl.release();
+  return TFFFT_OK;
+}
+
+int tffft_plan_workspace_bytes(tffft_plan_t pl, size_t* b) {
+  if (!pl || !b) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *b = pl->workspace;
+  return TFFFT_OK;
+}
+
+int tffft_plan_sizes(tffft_plan_t pl, int64_t* re, int64_t* sp) {
+  if (!pl || !re || !sp) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *re = (int64_t)pl->n0p * pl->n1 * pl->n2;
+  *sp = (int64_t)pl->n1p * pl->n0 * pl->n2c;
+  return TFFFT_OK;
+}
+
+static void free_events(tffft_plan_t pl) {
+  for (auto& ev : pl->events)
+    for (auto& e : ev.e) cudaEventDestroy(e);
+  pl->events.clear();
+}
+
+int tffft_plan_destroy(tffft_plan_t pl) {
+  if (!pl) return TFFFT_OK;
+  cudaSetDevice(pl->comm->device);
+  free_events(pl);
+  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
+  cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->pull_ptrs);
+  delete pl;
+  return TFFFT_OK;
+}
+
+static int check_ptr(const void* ptr, const char* what, size_t align) {
+  if (!ptr) return fail(TFFFT_ERR_CONTRACT, "%s is null", what);
+  if (reinterpret_cast<uintptr_t>(ptr) % align)
+    return fail(TFFFT_ERR_CONTRACT, "%s must be %zu-byte aligned", what, align);
+  return TFFFT_OK;
+}
+
+static int begin_events(tffft_plan_t pl, bool fwd, cudaStream_t s, StageEvents** ev) {
+  *ev = nullptr;
+  if (!pl->timing) return TFFFT_OK;
+  StageEvents e{};
+  e.forward = fwd;
+  for (auto& x : e.e) CUDA_TRY(cudaEventCreate(&x));
+  pl->events.push_back(e);
+  *ev = &pl->events.back();
+  CUDA_TRY(cudaEventRecord((*ev)->e[0], s));
+  return TFFFT_OK;
+}
+
+#define MARK(ev, i, s) \
+  if (ev) CUDA_TRY(cudaEventRecord((ev)->e[i], s));
+
+int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* stream) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  TRY(check_ptr(real_in, "real_in", pl->esz));
+  TRY(check_ptr(spec_out, "spec_out", pl->esz));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  StageEvents* ev;
+  TRY(begin_events(pl, true, s, &ev));
+  // stage 1: planes (dfft.py:161-163)
+  CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
+  TRY(fabric_guard_staging(pl, s));
+  TRY(stage1_columns(pl, spec_out, false, s));
+  MARK(ev, 1, s);
+  // exchange (exchange.py:263-276)
+  if (pl->p > 1 && !pl->comm->is_nccl) TRY(fabric_pull_list(pl, spec_out, s));
+  TRY(exchange(pl, spec_out, s));
+  MARK(ev, 2, s);
+  // stage 3: strided columns (dfft.py:170-171)
+  TRY(stage3_columns(pl, spec_out, false, s));
+  MARK(ev, 3, s);
+  return TFFFT_OK;
+}
+
+int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  TRY(check_ptr(spec, "spec_inout", pl->esz));
+  TRY(check_ptr(real_out, "real_out", pl->esz));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  StageEvents* ev;
+  TRY(begin_events(pl, false, s, &ev));
+  CUDA_TRY(cudaMemsetAsync(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p, s));
+  // stage 3' (dfft.py:196-197)
+  TRY(fabric_guard_staging(pl, s));
+  TRY(stage3_columns(pl, spec, true, s));
+  MARK(ev, 1, s);
+  // exchange (exchange.py:279-290)
+  if (pl->p > 1 && !pl->comm->is_nccl) TRY(fabric_pull_list(pl, spec, s));
+  TRY(exchange(pl, spec, s));
+  MARK(ev, 2, s);
+  // stage 1' (dfft.py:206-209)
+  TRY(stage1_columns(pl, spec, true, s));
+  CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+  MARK(ev, 3, s);
+  pl->last_inverse_stream = s;
+  pl->inverse_ran = true;
+  return TFFFT_OK;
+}
+
+int tffft_set_timing(tffft_plan_t pl, int enable) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  pl->timing = enable != 0;
+  return TFFFT_OK;
+}
+
+int tffft_stage_times(tffft_plan_t pl, double ms[3]) {
+  if (!pl || !ms) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  ms[0] = ms[1] = ms[2] = 0.0;
+  for (auto& ev : pl->events) {
+    CUDA_TRY(cudaEventSynchronize(ev.e[3]));
+    float a, b, c;
+    CUDA_TRY(cudaEventElapsedTime(&a, ev.e[0], ev.e[1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, ev.e[1], ev.e[2]));
+    CUDA_TRY(cudaEventElapsedTime(&c, ev.e[2], ev.e[3]));
+    // forward: stage1, exchange, stage3; inverse: stage3', exchange, stage1'
+    ms[ev.forward ? 0 : 2] += a;
+    ms[1] += b;
+    ms[ev.forward ? 2 : 0] += c;
+  }
+  return TFFFT_OK;
+}
+
+int tffft_counters(tffft_plan_t pl, uint64_t b[3]) {
+  if (!pl || !b) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  for (int i = 0; i < 3; ++i) b[i] = pl->counters[i];
+  return TFFFT_OK;
+}
+
+int tffft_reset_instrumentation(tffft_plan_t pl) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  free_events(pl);
+  pl->counters[0] = pl->counters[1] = pl->counters[2] = 0;
+  pl->launches = 0;
+  return TFFFT_OK;
+}
+
+int tffft_launch_count(tffft_plan_t pl, uint64_t* n) {
+  if (!pl || !n) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *n = pl->launches;
+  return TFFFT_OK;
+}
+
+int tffft_consistency(tffft_plan_t pl, double* residue) {
+  if (!pl || !residue) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *residue = 0.0;
+  if (!pl->inverse_ran) return TFFFT_OK;
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  CUDA_TRY(cudaStreamSynchronize(pl->last_inverse_stream));
+  std::vector<double> st(3 * (size_t)pl->n0p);
+  CUDA_TRY(cudaMemcpy(st.data(), pl->stats, st.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  double res = 0.0;
+  int bad = -1;
+  double bad_v = 0.0, bad_tol = 0.0;
+  for (int i = 0; i < pl->n0p; ++i) {
+    const double tol = 1e-9 * pl->n2 * std::sqrt(st[3 * i]);  // kernels.py:222-223
+    const double edge = st[3 * i + 1], r = st[3 * i + 2];
+    res = std::max(res, r);
+    if (bad < 0 && (edge > tol || r > tol)) {
+      bad = i;
+      bad_v = std::max(edge, r);
+      bad_tol = tol;
+    }
+  }
+  *residue = res;
+  if (bad >= 0)
+    return fail(TFFFT_ERR_CONSISTENCY,
+                "bins 0 and n/2 must be real for a half spectrum (plane %d: imag %.3e > %.3e)", bad, bad_v,
+                bad_tol);
+  return TFFFT_OK;
+}
+
+int tffft_exchange_schedule(int n0, int n1, int n2, int p, int rank, int64_t* ops, int64_t max_ops,
+                            int64_t* nops) {
+  if (!nops) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (p < 1 || rank < 0 || rank >= p || n0 % p || n1 % p)
+    return fail(TFFFT_ERR_CONFIGURATION, "invalid geometry");
+  const int64_t n0p = n0 / p, n1p = n1 / p, n2c = n2 / 2 + 1, chunk = n1p * n2c;
+  int64_t cnt = 0;
+  for (int d = 1; d < p; ++d) {
+    const int q = (rank + d) % p;
+    for (int64_t i = 0; i < n0p; ++i) {
+      if (ops && cnt < max_ops) {
+        ops[4 * cnt + 0] = q;
+        ops[4 * cnt + 1] = ((int64_t)q * n0p + i) * chunk;        // staging[q][i]
+        ops[4 * cnt + 2] = i * n1 * n2c + (int64_t)q * chunk;      // spectral band q of plane i
+        ops[4 * cnt + 3] = chunk;
+      }
+      ++cnt;
+    }
+  }
+  *nops = cnt;
+  if (ops && cnt > max_ops) return fail(TFFFT_ERR_CONFIGURATION, "ops buffer too small (%lld needed)", (long long)cnt);
+  return TFFFT_OK;
+}
+
+int tffft_radix_schedule(int log2n, int* radices, int* npasses) {
+  if (!npasses || log2n < 0 || log2n > kMaxLog) return fail(TFFFT_ERR_SIZE, "log2n out of range");
+  *npasses = num_passes(log2n);
+  if (radices)
+    for (int p = 0; p < *npasses; ++p) radices[p] = 1 << pass_bits(log2n, p);
+  return TFFFT_OK;
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

@@ -1,0 +1,177 @@
+"""Communicators for the GPU exchange (mirror of slabfft.transport's public
+surface, reference pkg/src/slabfft/transport.py:35-43, 425-468).
+
+Two backends behind one ``Endpoint``:
+
+LOCAL   p endpoints share an in-process fabric on ONE device; each rank is
+        driven by its own host thread (the reference's run_spmd model,
+        transport.py:433-468).  The exchange is a device-side pull of peer
+        chunks straight into the vacated STRIDED_INPLACE bands.
+NCCL    one process per GPU (torchrun); grouped ncclSend/ncclRecv over
+        NVLink/NVSwitch, chunk-granular landing in the same layout.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from enum import Enum
+
+import torch
+
+from . import _lib
+from .errors import ConfigurationError, TransportError
+
+__all__ = [
+    "CommMode",
+    "CommPattern",
+    "CopyCounter",
+    "Endpoint",
+    "make_communicators",
+    "run_spmd",
+    "init_nccl_endpoint",
+]
+
+
+class CommMode(Enum):
+    """Rank execution mode (transport.py:46-48).  On the GPU both run one
+    host thread per rank; SERIAL is accepted for API parity."""
+
+    THREADED = "threaded"
+    SERIAL = "serial"
+
+
+class CommPattern(Enum):
+    PAIRWISE = "pairwise"
+    COLLECTIVE = "collective"
+
+
+@dataclass
+class CopyCounter:
+    """Bytes moved by the three kinds of copy pass (transport.py:97-114)."""
+
+    bytes_packed: int = 0
+    bytes_wire: int = 0
+    bytes_unpacked: int = 0
+
+    def reset(self) -> None:
+        self.bytes_packed = self.bytes_wire = self.bytes_unpacked = 0
+
+    def total(self) -> int:
+        return self.bytes_packed + self.bytes_wire + self.bytes_unpacked
+
+    def snapshot(self) -> tuple[int, int, int]:
+        return (self.bytes_packed, self.bytes_wire, self.bytes_unpacked)
+
+
+class Endpoint:
+    """One rank's handle on the exchange fabric."""
+
+    def __init__(self, handle: int, rank: int, p: int, device: int, kind: str,
+                 host_barrier: threading.Barrier | None = None):
+        self._handle = ctypes.c_void_p(handle)
+        self.rank = rank
+        self.p = p
+        self.device = device
+        self.kind = kind
+        self._host_barrier = host_barrier
+        self._closed = False
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._closed:
+            raise TransportError("endpoint is closed")
+        return self._handle
+
+    def barrier(self) -> None:
+        """Device-complete barrier: drain this rank's stream, then meet the peers."""
+        torch.cuda.current_stream(self.device).synchronize()
+        if self.kind == "local":
+            if self._host_barrier is not None:
+                try:
+                    self._host_barrier.wait(timeout=600)
+                except threading.BrokenBarrierError as exc:
+                    raise TransportError("fabric aborted while waiting at barrier") from exc
+        elif self.p > 1 and torch.distributed.is_initialized():
+            torch.distributed.barrier()
+
+    def abort(self) -> None:
+        if self._host_barrier is not None:
+            self._host_barrier.abort()
+        _lib.check(_lib.lib().tffft_comm_abort(self._handle))
+
+    def close(self) -> None:
+        if not self._closed:
+            _lib.lib().tffft_comm_destroy(self._handle)
+            self._closed = True
+
+
+def make_communicators(p: int, mode: CommMode = CommMode.THREADED, device: int | None = None,
+                       timeout: float = 600.0) -> list[Endpoint]:
+    """p connected endpoints sharing one in-process fabric on one GPU
+    (transport.py:425-430)."""
+    if p < 1:
+        raise ConfigurationError(f"communicator group needs p >= 1, got {p}")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    arr = (ctypes.c_void_p * p)()
+    _lib.check(_lib.lib().tffft_comm_init_local(p, dev, arr))
+    bar = threading.Barrier(p)
+    return [Endpoint(arr[r], r, p, dev, "local", bar) for r in range(p)]
+
+
+def run_spmd(p: int, fn, mode: CommMode = CommMode.THREADED, device: int | None = None,
+             timeout: float = 600.0) -> list:
+    """Run fn(endpoint) on p ranks (one host thread each) and return the
+    results in rank order; the first failure aborts the fabric and is
+    re-raised (transport.py:433-468)."""
+    eps = make_communicators(p, mode, device, timeout)
+    results: list = [None] * p
+    errors: list[BaseException | None] = [None] * p
+    dev = eps[0].device
+
+    def body(rank: int) -> None:
+        try:
+            torch.cuda.set_device(dev)
+            results[rank] = fn(eps[rank])
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            errors[rank] = exc
+            eps[rank].abort()
+
+    threads = [threading.Thread(target=body, args=(r,), name=f"rank{r}") for r in range(p)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for ep in eps:
+        ep.close()
+    primary = next((e for e in errors if e is not None and not isinstance(e, TransportError)), None)
+    if primary is None:
+        primary = next((e for e in errors if e is not None), None)
+    if primary is not None:
+        raise primary
+    return results
+
+
+def init_nccl_endpoint(device: int | None = None) -> Endpoint:
+    """Endpoint for this process of a torch.distributed job (torchrun): the
+    NCCL unique id is created on rank 0 and broadcast through the default
+    process group (gloo or nccl)."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise ConfigurationError("torch.distributed is not initialised")
+    rank, p = dist.get_rank(), dist.get_world_size()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    uid = bytearray(128)
+    if p > 1:
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            _lib.check(_lib.lib().tffft_get_unique_id(buf))
+            uid = bytearray(buf.raw)
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = bytearray(obj[0])
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().tffft_comm_init_rank(p, rank, bytes(uid), dev, ctypes.byref(h)))
+    return Endpoint(h.value, rank, p, dev, "nccl")

@@ -1,0 +1,153 @@
+"""GPU parity: libtffft forward/inverse against the CPU oracle (bit-pinned to
+the reference) on seeded inputs.  Tolerances (BASELINE.json north_star):
+relative L2 <= 1e-12 for float64, <= 1e-5 for float32, for the forward
+spectrum and for the forward->inverse round trip."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1406_5597_b200 as tf
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"float64": 1e-12, "float32": 1e-5}
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def run_pair(x, p, dtype="float64"):
+    """forward + inverse on p ranks of the local fabric; returns per-rank flat
+    spectral buffers (numpy), per-rank real outputs (numpy), residue."""
+    shape = x.shape
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dtype)
+        spec = tf.forward(fp, slabs[ep.rank])
+        f = spec.data.cpu().numpy().copy()
+        back = tf.inverse(fp, spec)
+        return f, back.data.cpu().numpy().copy(), fp.last_imag_residue
+
+    res = tf.run_spmd(p, body)
+    return [r[0] for r in res], [r[1] for r in res], max(r[2] for r in res)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "ref_*.npz"))),
+                         ids=lambda s: os.path.basename(s))
+def test_golden_reference_vectors(path):
+    """The GPU result against the reference's own outputs (fixtures)."""
+    d = np.load(path)
+    n0, n1, n2 = (int(v) for v in d["shape"])
+    p = int(d["p"])
+    gen = oracle.uniform_field if str(d["dist"]) == "uniform" else oracle.normal_field
+    x = gen((n0, n1, n2), int(d["seed"]))
+    fwd, inv, _ = run_pair(x, p)
+    for q in range(p):
+        assert rel(fwd[q], d["fwd"][q]) <= 1e-12
+        assert rel(inv[q], d["inv"][q]) <= 1e-12
+
+
+GRIDS = [
+    ((2, 2, 2), 1), ((2, 2, 2), 2), ((4, 4, 4), 4), ((8, 8, 8), 1), ((16, 16, 16), 2),
+    ((64, 64, 64), 1), ((32, 64, 128), 4), ((128, 16, 32), 8), ((16, 256, 64), 2),
+    ((8, 8, 2048), 1), ((8, 2048, 4), 2), ((2048, 4, 8), 4), ((4096, 2, 2), 1), ((2, 4096, 4), 2),
+    ((4, 4, 4096), 1), ((512, 8, 16), 8),
+]
+
+
+@pytest.mark.parametrize("shape,p", GRIDS, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_forward_inverse_vs_oracle(shape, p, dtype):
+    x = oracle.uniform_field(shape, seed=sum(shape) + p)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)  # identical values for both sides
+    ref_flats = oracle.forward_all(x, p)
+    fwd, inv, _ = run_pair(x, p, dtype)
+    ref = oracle.gather_spectral(ref_flats, shape)
+    got = oracle.gather_spectral([f.astype(np.complex128) for f in fwd], shape)
+    assert rel(got, ref) <= TOL[dtype]
+    # per-rank buffers are in the reference's STRIDED_INPLACE layout
+    for q in range(p):
+        assert rel(fwd[q], ref_flats[q]) <= TOL[dtype]
+    back = np.concatenate([r.reshape(-1) for r in inv]).reshape(shape)
+    assert rel(back, x) <= TOL[dtype]
+
+
+def test_128_cubed_p2_layout_and_roundtrip():
+    """BASELINE config 2: 128^3 float64 uniform, p=2: strided exchange layout + round trip."""
+    shape = (128, 128, 128)
+    x = oracle.uniform_field(shape, seed=2)
+    ref_flats = oracle.forward_all(x, 2)
+    fwd, inv, _ = run_pair(x, 2)
+    for q in range(2):
+        assert rel(fwd[q], ref_flats[q]) <= 1e-12
+    assert rel(np.concatenate([r.reshape(-1) for r in inv]).reshape(shape), x) <= 1e-12
+
+
+def test_64_cubed_p1_elementwise():
+    """BASELINE config 1: 64^3 float64 uniform, p=1, elementwise vs the oracle."""
+    shape = (64, 64, 64)
+    x = oracle.uniform_field(shape, seed=1)
+    ref = oracle.forward_all(x, 1)[0]
+    fwd, inv, _ = run_pair(x, 1)
+    assert np.max(np.abs(fwd[0] - ref)) <= 1e-10 * np.max(np.abs(ref))
+    assert np.max(np.abs(inv[0].reshape(shape) - x)) <= 1e-13
+
+
+def test_inverse_rejects_non_hermitian_spectrum():
+    """kernels.py:225-238: imaginary DC/Nyquist bins raise ConsistencyError."""
+    shape = (8, 8, 8)
+    grid = tf.GlobalGrid(*shape)
+    ep = tf.make_communicators(1)[0]
+    fp = tf.plan(grid, ep)
+    x = oracle.uniform_field(shape, 3)
+    spec = tf.forward(fp, tf.scatter_real(x, grid, 1)[0])
+    v = spec.data.view(8, 8, 5)
+    v[1, 2, 0] += 1j  # DC bin of one row becomes non-real
+    with pytest.raises(tf.ConsistencyError):
+        tf.inverse(fp, spec)
+
+
+def test_contract_errors():
+    grid = tf.GlobalGrid(8, 8, 8)
+    ep = tf.make_communicators(1)[0]
+    fp = tf.plan(grid, ep)
+    other = tf.scatter_real(np.zeros((8, 8, 8)), grid, 1, dtype="float32")[0]
+    with pytest.raises(tf.ContractError):
+        tf.forward(fp, other)
+    spec = tf.SpectralSlab(fp.spectral_layout, tf.SpectralTag.CONTIGUOUS_FLIPPED, fp.work1)
+    with pytest.raises(tf.ContractError):
+        tf.inverse(fp, spec)
+
+
+def test_counters_and_timers():
+    shape = (16, 16, 16)
+    x = oracle.uniform_field(shape, 5)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, 4)
+
+    def body(ep):
+        fp = tf.plan(grid, ep)
+        fp.enable_timing()
+        fp.reset_instrumentation()
+        tf.inverse(fp, tf.forward(fp, slabs[ep.rank]))
+        return fp.counters.snapshot(), fp.timers_us, fp.launches
+
+    res = tf.run_spmd(4, body)
+    chunk = 16 // 4 * 16 // 4 * 9 * 16
+    for snap, timers, launches in res:
+        # STRIDED: no pack / unpack pass, wire = off-rank bytes of two exchanges (transport.py:343-344)
+        assert snap == (0, 2 * 3 * chunk, 0)
+        assert set(timers) == {"stage1_us", "exchange_us", "stage3_us"}
+        assert all(v >= 0 for v in timers.values())
+        assert launches >= 6
