@@ -39,13 +39,13 @@ __host__ __device__ constexpr int ept_bits(int L) { return L == 0 ? 0 : pass_bit
 __host__ __device__ constexpr int ns_bits(int L, int p) {
   return p == 0 ? 0 : ns_bits(L, p - 1) + pass_bits(L, p - 1);
 }
-// offset of pass p's twiddle block (passes >= 1 only); block p holds Ns*R entries
+// offset of pass p's twiddle block (passes >= 1 only); block p holds the Ns
+// roots exp(-2 pi i k / (Ns R)), k < Ns; powers m = 2..R-1 are formed in registers
 __host__ __device__ constexpr int tw_offset(int L, int p) {
-  return p <= 1 ? 0 : tw_offset(L, p - 1) + (1 << (ns_bits(L, p - 1) + pass_bits(L, p - 1)));
+  return p <= 1 ? 0 : tw_offset(L, p - 1) + (1 << ns_bits(L, p - 1));
 }
 __host__ __device__ constexpr int tw_total(int L) {
-  return num_passes(L) <= 1 ? 0 : tw_offset(L, num_passes(L) - 1) +
-      (1 << (ns_bits(L, num_passes(L) - 1) + pass_bits(L, num_passes(L) - 1)));
+  return num_passes(L) <= 1 ? 0 : tw_offset(L, num_passes(L) - 1) + (1 << ns_bits(L, num_passes(L) - 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -84,6 +84,25 @@ template <typename T>
 __device__ __forceinline__ cx<T> ldg_cx(const cx<T>* p) {
   auto v = __ldg(reinterpret_cast<const typename vec2<T>::type*>(p));
   return {v.x, v.y};
+}
+
+// w^m for m = 1..R-1 by a balanced product tree (depth <= log2 R), from one
+// table load instead of R-1: trades L1 wavefronts for idle FP64 issue slots.
+__host__ __device__ constexpr int hibit(int m) { return m < 2 ? m : 2 * hibit(m / 2); }
+
+template <int M, int R, typename T>
+__device__ __forceinline__ void twiddle_powers_from(cx<T>* pw) {
+  if constexpr (M < R) {
+    constexpr int HI = hibit(M);
+    if constexpr (M == HI) pw[M] = cmul(pw[M / 2], pw[M / 2]);
+    else pw[M] = cmul(pw[HI], pw[M - HI]);
+    twiddle_powers_from<M + 1, R>(pw);
+  }
+}
+template <int R, typename T>
+__device__ __forceinline__ void twiddle_powers(cx<T> w, cx<T>* pw) {
+  pw[1] = w;
+  twiddle_powers_from<2, R>(pw);
 }
 
 // ---------------------------------------------------------------------------
@@ -198,9 +217,10 @@ struct Stockham {
       if constexpr (p > 0) {
         const int j = tt + TPT * u;
         const int k = j & (NS - 1);
-        const cx<T>* t = tw + tw_offset(L, p) + k * R;
+        cx<T> pw[R];
+        twiddle_powers<R>(ldg_cx(tw + tw_offset(L, p) + k), pw);
 #pragma unroll
-        for (int m = 1; m < R; ++m) v[u * R + m] = ctw<INV>(v[u * R + m], ldg_cx(t + m));
+        for (int m = 1; m < R; ++m) v[u * R + m] = ctw<INV>(v[u * R + m], pw[m]);
       }
       DFT<R, INV, T>::run(v + u * R);
     }

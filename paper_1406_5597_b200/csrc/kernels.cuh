@@ -45,12 +45,18 @@ struct RowParams {
   unsigned long long* stats;      // c2r: per plane [m2, edge, residue] as ordered doubles
 };
 
-template <int L> struct ColCfg {
+// Column smem layout: one pad slot per E elements inside a column (so the
+// stride-R writes of the first pass spread over banks) and a column stride S
+// with S*sizeof(cx) == 32 mod 128 bytes, so the B=4 adjacent columns of an
+// LDS/STS wavefront start in disjoint bank quarters.
+template <typename T, int L> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
   static constexpr int B = L >= 12 ? 2 : (256 / TPT > 4 ? 256 / TPT : 4);
   static constexpr int THREADS = TPT * B;
-  static constexpr int S = Shape<L>::N + 1;  // odd row stride: 8 adjacent columns hit 8 bank groups
-  static constexpr int PS = 30;              // no in-row padding
+  static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
+  static constexpr int Q = 128 / (int)sizeof(cx<T>);  // elements per 128 bytes
+  static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
+  static constexpr int S = ((RAW + Q - 1) / Q) * Q + Q / 4;
   static constexpr bool SMEM = Shape<L>::P > 1;
 };
 
@@ -65,7 +71,7 @@ template <int L> struct RowCfg {
 
 template <typename T, int L>
 __host__ __device__ constexpr size_t col_smem_bytes() {
-  return ColCfg<L>::SMEM ? sizeof(cx<T>) * ColCfg<L>::B * ColCfg<L>::S : 0;
+  return ColCfg<T, L>::SMEM ? sizeof(cx<T>) * ColCfg<T, L>::B * ColCfg<T, L>::S : 0;
 }
 template <typename T, int L>
 __host__ __device__ constexpr size_t row_smem_bytes() {
@@ -76,9 +82,9 @@ __host__ __device__ constexpr size_t row_smem_bytes() {
 // batched column c2c (stages 1b, 3, 3', 1b')
 // ---------------------------------------------------------------------------
 template <typename T, int L, bool INV>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+__global__ void __launch_bounds__(ColCfg<T, L>::THREADS)
 col_fft_kernel(const ColParams prm) {
-  using CF = ColCfg<L>;
+  using CF = ColCfg<T, L>;
   using SH = Shape<L>;
   using ST = Stockham<T, L, INV, CF::S, CF::PS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];

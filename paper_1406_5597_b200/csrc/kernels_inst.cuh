@@ -12,7 +12,7 @@ static cudaError_t prep_smem(K kernel, size_t bytes) {
 
 template <typename T, int L, bool INV>
 static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
-  using CF = ColCfg<L>;
+  using CF = ColCfg<T, L>;
   const size_t sm = col_smem_bytes<T, L>();
   auto k = col_fft_kernel<T, L, INV>;
   static cudaError_t prep = prep_smem(k, sm);
