@@ -81,7 +81,12 @@ __host__ __device__ constexpr size_t row_smem_bytes() {
 // ---------------------------------------------------------------------------
 // batched column c2c (stages 1b, 3, 3', 1b')
 // ---------------------------------------------------------------------------
-template <typename T, int L, bool INV>
+// TWO   : element offsets use the two-level STRIDED_INPLACE formula (p > 1,
+//         stage 3); otherwise offset = e * inner_stride.
+// REDIR : epilogue sends peer bands to the exchange staging buffer.
+// All element offsets are 32-bit (plan_create bounds the slab below 2^32
+// elements); the 64-bit column base pointer is formed once per thread.
+template <typename T, int L, bool INV, bool TWO, bool REDIR>
 __global__ void __launch_bounds__(ColCfg<T, L>::THREADS)
 col_fft_kernel(const ColParams prm) {
   using CF = ColCfg<T, L>;
@@ -90,49 +95,52 @@ col_fft_kernel(const ColParams prm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
   const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
-  cx<T>* data = reinterpret_cast<cx<T>*>(prm.data);
 
   const int b = threadIdx.x % CF::B;
   const int tt = threadIdx.x / CF::B;
-  const long long c = (long long)blockIdx.x * CF::B + b;
-  const bool valid = c < prm.ncols;
-  const unsigned cq = valid ? (unsigned)(c / prm.cpb) : 0u;
-  const unsigned cr = valid ? (unsigned)(c - (long long)cq * prm.cpb) : 0u;
-  const long long base = (long long)cq * prm.grp_stride + cr;
-  const int icm = (1 << prm.ic_shift) - 1;
+  const long long c_raw = (long long)blockIdx.x * CF::B + b;
+  const bool valid = c_raw < prm.ncols;
+  const unsigned c = (unsigned)(valid ? c_raw : prm.ncols - 1);  // clamp: loads stay in bounds
+  const unsigned cq = c / (unsigned)prm.cpb;
+  const unsigned cr = c - cq * (unsigned)prm.cpb;
+  cx<T>* col = reinterpret_cast<cx<T>*>(prm.data) + ((long long)cq * prm.grp_stride + cr);
+  const unsigned is = (unsigned)prm.inner_stride;
+  const unsigned bs = (unsigned)prm.block_stride;
+  const unsigned icm = (1u << prm.ic_shift) - 1u;
+
+  auto offset = [&](unsigned e) -> unsigned {
+    if constexpr (TWO) return (e & icm) * is + (e >> prm.ic_shift) * bs;
+    else return e * is;
+  };
 
   cx<T> v[SH::E];
 #pragma unroll
   for (int u = 0; u < SH::E / SH::R0; ++u)
 #pragma unroll
-    for (int m = 0; m < SH::R0; ++m) {
-      const int e = SH::in_elem(tt, u, m);
-      const long long off = base + (long long)(e & icm) * prm.inner_stride +
-                            (long long)(e >> prm.ic_shift) * prm.block_stride;
-      v[u * SH::R0 + m] = valid ? data[off] : cx<T>{T(0), T(0)};
-    }
+    for (int m = 0; m < SH::R0; ++m) v[u * SH::R0 + m] = col[offset(SH::in_elem(tt, u, m))];
 
   ST::run(sm, v, tt, b, tw);
 
   if (!valid) return;
-  cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging);
-  const int bmask = (1 << prm.band_shift) - 1;
+  if constexpr (REDIR) {
+    cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging) + ((long long)cq * prm.stg_grp + cr);
+    const unsigned bmask = (1u << prm.band_shift) - 1u;
+    const unsigned sb = (unsigned)prm.stg_band, sw = (unsigned)prm.stg_within;
 #pragma unroll
-  for (int u = 0; u < SH::E / SH::RL; ++u)
+    for (int u = 0; u < SH::E / SH::RL; ++u)
 #pragma unroll
-    for (int m = 0; m < SH::RL; ++m) {
-      const int e = SH::out_elem(tt, u, m);
-      const int band = e >> prm.band_shift;
-      if (stg != nullptr && band != prm.self_band) {
-        const long long off = (long long)band * prm.stg_band + (long long)(e & bmask) * prm.stg_within +
-                              (long long)cq * prm.stg_grp + cr;
-        stg[off] = v[u * SH::RL + m];
-      } else {
-        const long long off = base + (long long)(e & icm) * prm.inner_stride +
-                              (long long)(e >> prm.ic_shift) * prm.block_stride;
-        data[off] = v[u * SH::RL + m];
+      for (int m = 0; m < SH::RL; ++m) {
+        const unsigned e = SH::out_elem(tt, u, m);
+        const int band = (int)(e >> prm.band_shift);
+        if (band != prm.self_band) stg[band * sb + (e & bmask) * sw] = v[u * SH::RL + m];
+        else col[offset(e)] = v[u * SH::RL + m];
       }
-    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < SH::E / SH::RL; ++u)
+#pragma unroll
+      for (int m = 0; m < SH::RL; ++m) col[offset(SH::out_elem(tt, u, m))] = v[u * SH::RL + m];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -279,8 +287,9 @@ c2r_rows_kernel(const RowParams prm) {
 }
 
 // host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)
+// variant: 0 = single stride, 1 = single stride + redirect, 2 = two-level, 3 = two-level + redirect
 template <typename T>
-cudaError_t launch_col_fft(int L, bool inv, const ColParams& p, cudaStream_t s);
+cudaError_t launch_col_fft(int L, bool inv, int variant, const ColParams& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_r2c_rows(int L, const RowParams& p, cudaStream_t s);
 template <typename T>

@@ -10,11 +10,11 @@ static cudaError_t prep_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <typename T, int L, bool INV>
+template <typename T, int L, bool INV, bool TWO, bool REDIR>
 static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   using CF = ColCfg<T, L>;
   const size_t sm = col_smem_bytes<T, L>();
-  auto k = col_fft_kernel<T, L, INV>;
+  auto k = col_fft_kernel<T, L, INV, TWO, REDIR>;
   static cudaError_t prep = prep_smem(k, sm);
   if (prep != cudaSuccess) return prep;
   const long long blocks = (p.ncols + CF::B - 1) / CF::B;
@@ -49,13 +49,31 @@ static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// instantiated variants: stage 1b fwd (+redirect), stage 1b' inv, stage 3 fwd
+// (single / two-level), stage 3' inv (single / two-level + redirect)
+template <typename T, int L>
+static cudaError_t col_dispatch(bool inv, int variant, const ColParams& p, cudaStream_t s) {
+  if (!inv) {
+    switch (variant) {
+      case 0: return col_one<T, L, false, false, false>(p, s);
+      case 1: return col_one<T, L, false, false, true>(p, s);
+      case 2: return col_one<T, L, false, true, false>(p, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (variant) {
+    case 0: return col_one<T, L, true, false, false>(p, s);
+    case 3: return col_one<T, L, true, true, true>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 #define TFFFT_COL_CASE(LL) \
-  case LL: return inv ? col_one<TFFFT_REAL, LL, true>(p, s) : col_one<TFFFT_REAL, LL, false>(p, s);
+  case LL: return col_dispatch<TFFFT_REAL, LL>(inv, variant, p, s);
 #define TFFFT_ROW_CASE(LL, FN) \
   case LL: return FN<TFFFT_REAL, LL>(p, s);
 
 template <>
-cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, const ColParams& p, cudaStream_t s) {
+cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, int variant, const ColParams& p, cudaStream_t s) {
   switch (L) {
     TFFFT_COL_CASE(1) TFFFT_COL_CASE(2) TFFFT_COL_CASE(3) TFFFT_COL_CASE(4)
     TFFFT_COL_CASE(5) TFFFT_COL_CASE(6) TFFFT_COL_CASE(7) TFFFT_COL_CASE(8)

@@ -261,10 +261,11 @@ static int upload_table(const std::vector<double>& t, int dtype, void** dev, siz
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 // ---------------------------------------------------------------------------
-static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, const ColParams& prm, cudaStream_t s) {
+static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, int variant, const ColParams& prm,
+                              cudaStream_t s) {
   pl->launches++;
-  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, prm, s)
-                                : launch_col_fft<float>(L, inv, prm, s);
+  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, variant, prm, s)
+                                : launch_col_fft<float>(L, inv, variant, prm, s);
 }
 static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
@@ -313,7 +314,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
   }
-  CUDA_TRY(col_launch(pl, pl->L1, inv, c, s));
+  CUDA_TRY(col_launch(pl, pl->L1, inv, c.staging ? 1 : 0, c, s));
   return TFFFT_OK;
 }
 
@@ -338,7 +339,7 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.stg_within = (long long)pl->n1p * pl->n2c;
     c.stg_grp = 0;
   }
-  CUDA_TRY(col_launch(pl, pl->L0, inv, c, s));
+  CUDA_TRY(col_launch(pl, pl->L0, inv, pl->p == 1 ? 0 : (c.staging ? 3 : 2), c, s));
   return TFFFT_OK;
 }
 
@@ -549,6 +550,10 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
   if (n0 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n0 (%d does not divide %d)", p, n0);
   if (n1 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n1 (%d does not divide %d)", p, n1);
   if (dtype != TFFFT_F64 && dtype != TFFFT_F32) return fail(TFFFT_ERR_CONFIGURATION, "unknown dtype %d", dtype);
+  // kernels address the local spectral slab with 32-bit element offsets
+  if ((long long)(n0 / p) * n1 * (n2 / 2 + 1) >= (1LL << 32))
+    return fail(TFFFT_ERR_SIZE, "local slab of %lld complex elements exceeds 2^32; use more ranks",
+                (long long)(n0 / p) * n1 * (n2 / 2 + 1));
   if (pattern != TFFFT_PAIRWISE)
     return fail(TFFFT_ERR_CONFIGURATION, "only the PAIRWISE comm pattern is implemented on the GPU");
 
