@@ -183,9 +183,22 @@ struct DFT<4, INV, T> {
 };
 
 // ---------------------------------------------------------------------------
+// async copy helpers (LDGSTS)
+// ---------------------------------------------------------------------------
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // Stockham pass machinery
 // ---------------------------------------------------------------------------
-// SMEM index policy: element a of transform b lives at b*S + a + (a >> PS).
 template <int L>
 struct Shape {
   static constexpr int N = 1 << L;
@@ -199,9 +212,14 @@ struct Shape {
   // element index held in v[u*R0+m] before pass 0 / in v[u*RL+m] after the last pass
   static __device__ __forceinline__ int in_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / R0); }
   static __device__ __forceinline__ int out_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / RL); }
+  // register slot of pass-0 input element tt + TPT*k (k < E)
+  static __device__ __forceinline__ constexpr int in_slot(int k) { return (k % (E / R0)) * R0 + k / (E / R0); }
 };
 
-template <typename T, int L, bool INV, int S, int PS>
+// Exchange buffer: element a of transform b at b*S + a + (a >> PS).  With
+// SPLIT (float64) the exchange runs in two rounds of 8-byte words (real parts,
+// then imaginary parts), halving the buffer; otherwise whole complex values.
+template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false>
 struct Stockham {
   using SH = Shape<L>;
   static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;
@@ -226,8 +244,21 @@ struct Stockham {
     }
   }
 
-  template <int p>
-  static __device__ __forceinline__ void store(cx<T>* sm, const cx<T>* v, int tt, int b) {
+  // COMP: 0 = real part, 1 = imaginary part, 2 = whole complex value
+  template <int COMP>
+  static __device__ __forceinline__ void put(void* sm, int i, const cx<T>& x) {
+    if constexpr (COMP == 2) reinterpret_cast<cx<T>*>(sm)[i] = x;
+    else reinterpret_cast<T*>(sm)[i] = COMP == 0 ? x.x : x.y;
+  }
+  template <int COMP>
+  static __device__ __forceinline__ void get(const void* sm, int i, cx<T>& x) {
+    if constexpr (COMP == 2) x = reinterpret_cast<const cx<T>*>(sm)[i];
+    else if constexpr (COMP == 0) x.x = reinterpret_cast<const T*>(sm)[i];
+    else x.y = reinterpret_cast<const T*>(sm)[i];
+  }
+
+  template <int p, int COMP>
+  static __device__ __forceinline__ void store(void* sm, const cx<T>* v, int tt, int b) {
     constexpr int R = 1 << pass_bits(L, p);
     constexpr int NS = 1 << ns_bits(L, p);
 #pragma unroll
@@ -235,29 +266,44 @@ struct Stockham {
       const int j = tt + TPT * u;
       const int base = (j / NS) * NS * R + (j & (NS - 1));
 #pragma unroll
-      for (int m = 0; m < R; ++m) sm[sidx(b, base + m * NS)] = v[u * R + m];
+      for (int m = 0; m < R; ++m) put<COMP>(sm, sidx(b, base + m * NS), v[u * R + m]);
     }
   }
 
-  template <int p>
-  static __device__ __forceinline__ void load(const cx<T>* sm, cx<T>* v, int tt, int b) {
+  template <int p, int COMP>
+  static __device__ __forceinline__ void load(const void* sm, cx<T>* v, int tt, int b) {
     constexpr int R = 1 << pass_bits(L, p);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       const int j = tt + TPT * u;
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[u * R + m] = sm[sidx(b, j + m * (N / R))];
+      for (int m = 0; m < R; ++m) get<COMP>(sm, sidx(b, j + m * (N / R)), v[u * R + m]);
     }
   }
 
   template <int p>
-  static __device__ __forceinline__ void rest(cx<T>* sm, cx<T>* v, int tt, int b,
-                                              const cx<T>* __restrict__ tw) {
+  static __device__ __forceinline__ void exchange(void* sm, cx<T>* v, int tt, int b) {
+    if constexpr (SPLIT) {
+      store<p - 1, 0>(sm, v, tt, b);
+      __syncthreads();
+      load<p, 0>(sm, v, tt, b);
+      __syncthreads();
+      store<p - 1, 1>(sm, v, tt, b);
+      __syncthreads();
+      load<p, 1>(sm, v, tt, b);
+      __syncthreads();
+    } else {
+      store<p - 1, 2>(sm, v, tt, b);
+      __syncthreads();
+      load<p, 2>(sm, v, tt, b);
+      __syncthreads();
+    }
+  }
+
+  template <int p>
+  static __device__ __forceinline__ void rest(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
     if constexpr (p < P) {
-      store<p - 1>(sm, v, tt, b);
-      __syncthreads();
-      load<p>(sm, v, tt, b);
-      __syncthreads();
+      exchange<p>(sm, v, tt, b);
       compute<p>(v, tt, tw);
       rest<p + 1>(sm, v, tt, b, tw);
     }
@@ -265,17 +311,20 @@ struct Stockham {
 
   // v holds pass-0 inputs (element in_elem(tt,u,m) in v[u*R0+m]); on return
   // v[u*RL+m] holds output element out_elem(tt,u,m).  All threads of the CTA
-  // must call this (it synchronises when P > 1).
-  static __device__ __forceinline__ void run(cx<T>* sm, cx<T>* v, int tt, int b,
-                                             const cx<T>* __restrict__ tw) {
-    if constexpr (P > 0) {
-      compute<0>(v, tt, tw);
-      rest<1>(sm, v, tt, b, tw);
-    }
+  // must call this (it synchronises when P > 1).  run = first() + finish().
+  static __device__ __forceinline__ void first(cx<T>* v, int tt, const cx<T>* __restrict__ tw) {
+    if constexpr (P > 0) compute<0>(v, tt, tw);
+  }
+  static __device__ __forceinline__ void finish(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
+    if constexpr (P > 0) rest<1>(sm, v, tt, b, tw);
+  }
+  static __device__ __forceinline__ void run(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
+    first(v, tt, tw);
+    finish(sm, v, tt, b, tw);
   }
 
   // write the final outputs into smem at their natural index (for the real
-  // transforms' post-processing that pairs bins k and N-k)
+  // transforms' post-processing that pairs bins k and N-k); whole complex values
   static __device__ __forceinline__ void store_natural(cx<T>* sm, const cx<T>* v, int tt, int b) {
     constexpr int RL = SH::RL;
 #pragma unroll

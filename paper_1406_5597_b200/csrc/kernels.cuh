@@ -45,19 +45,23 @@ struct RowParams {
   unsigned long long* stats;      // c2r: per plane [m2, edge, residue] as ordered doubles
 };
 
-// Column smem layout: one pad slot per E elements inside a column (so the
-// stride-R writes of the first pass spread over banks) and a column stride S
-// with S*sizeof(cx) == 32 mod 128 bytes, so the B=4 adjacent columns of an
-// LDS/STS wavefront start in disjoint bank quarters.
+// Column CTA: B adjacent columns, TPT threads per column, E elements per
+// thread.  Shared memory = the prefetch slots P (THREADS*E complex, each
+// thread's own slots) + the exchange buffer X in 8-byte words (float64 splits
+// its complex values into two rounds).  X layout: one pad word per E words
+// inside a column, column stride S == 4 mod 16 words, so the 16 lanes of an
+// 8-byte LDS/STS wavefront (4 columns x 4 threads) hit 16 distinct bank pairs.
 template <typename T, int L> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
   static constexpr int B = L >= 12 ? 2 : (256 / TPT > 4 ? 256 / TPT : 4);
   static constexpr int THREADS = TPT * B;
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
-  static constexpr int Q = 128 / (int)sizeof(cx<T>);  // elements per 128 bytes
   static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
-  static constexpr int S = ((RAW + Q - 1) / Q) * Q + Q / 4;
-  static constexpr bool SMEM = Shape<L>::P > 1;
+  static constexpr int S = ((RAW + 15) / 16) * 16 + 4;
+  static constexpr bool SPLIT = sizeof(T) == 8;
+  static constexpr bool XCHG = Shape<L>::P > 1;
+  static constexpr size_t P_BYTES = sizeof(cx<T>) * THREADS * Shape<L>::E;
+  static constexpr size_t X_BYTES = XCHG ? 8 * (size_t)B * S : 0;
 };
 
 template <int L> struct RowCfg {
@@ -71,7 +75,7 @@ template <int L> struct RowCfg {
 
 template <typename T, int L>
 __host__ __device__ constexpr size_t col_smem_bytes() {
-  return ColCfg<T, L>::SMEM ? sizeof(cx<T>) * ColCfg<T, L>::B * ColCfg<T, L>::S : 0;
+  return ColCfg<T, L>::P_BYTES + ColCfg<T, L>::X_BYTES;
 }
 template <typename T, int L>
 __host__ __device__ constexpr size_t row_smem_bytes() {
@@ -79,67 +83,97 @@ __host__ __device__ constexpr size_t row_smem_bytes() {
 }
 
 // ---------------------------------------------------------------------------
-// batched column c2c (stages 1b, 3, 3', 1b')
+// batched column c2c (stages 1b, 3, 3', 1b') -- persistent, prefetching
 // ---------------------------------------------------------------------------
+// Each CTA walks tiles blockIdx.x, +gridDim.x, ...  While tile i is being
+// transformed out of registers, tile i+1 streams into the thread-private
+// prefetch slots with cp.async: every thread copies exactly the E elements it
+// will feed into pass 0, so the hand-off needs no CTA barrier.
 // TWO   : element offsets use the two-level STRIDED_INPLACE formula (p > 1,
 //         stage 3); otherwise offset = e * inner_stride.
 // REDIR : epilogue sends peer bands to the exchange staging buffer.
 // All element offsets are 32-bit (plan_create bounds the slab below 2^32
-// elements); the 64-bit column base pointer is formed once per thread.
+// elements); the 64-bit column base pointer is formed once per tile.
 template <typename T, int L, bool INV, bool TWO, bool REDIR>
 __global__ void __launch_bounds__(ColCfg<T, L>::THREADS)
 col_fft_kernel(const ColParams prm) {
   using CF = ColCfg<T, L>;
   using SH = Shape<L>;
-  using ST = Stockham<T, L, INV, CF::S, CF::PS>;
+  using ST = Stockham<T, L, INV, CF::S, CF::PS, CF::SPLIT>;
+  constexpr int E = SH::E, TPT = SH::TPT, B = CF::B, NT = CF::THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+  cx<T>* pf = reinterpret_cast<cx<T>*>(smem_raw);  // [E][NT] prefetch slots
+  void* xs = smem_raw + CF::P_BYTES;               // exchange buffer
   const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
 
-  const int b = threadIdx.x % CF::B;
-  const int tt = threadIdx.x / CF::B;
-  const long long c_raw = (long long)blockIdx.x * CF::B + b;
-  const bool valid = c_raw < prm.ncols;
-  const unsigned c = (unsigned)(valid ? c_raw : prm.ncols - 1);  // clamp: loads stay in bounds
-  const unsigned cq = c / (unsigned)prm.cpb;
-  const unsigned cr = c - cq * (unsigned)prm.cpb;
-  cx<T>* col = reinterpret_cast<cx<T>*>(prm.data) + ((long long)cq * prm.grp_stride + cr);
+  const int t = threadIdx.x;
+  const int b = t % B;
+  const int tt = t / B;
   const unsigned is = (unsigned)prm.inner_stride;
   const unsigned bs = (unsigned)prm.block_stride;
-  const unsigned icm = (1u << prm.ic_shift) - 1u;
+  const unsigned ics = (unsigned)prm.ic_shift;
+  const unsigned icm = (1u << ics) - 1u;
+  const long long ntiles = (prm.ncols + B - 1) / B;
 
   auto offset = [&](unsigned e) -> unsigned {
-    if constexpr (TWO) return (e & icm) * is + (e >> prm.ic_shift) * bs;
+    if constexpr (TWO) return (e & icm) * is + (e >> ics) * bs;
     else return e * is;
   };
+  struct Col { cx<T>* p; unsigned cq, cr; bool valid; };
+  auto column = [&](long long tile) -> Col {
+    const long long c_raw = tile * B + b;
+    const bool valid = c_raw < prm.ncols;
+    const unsigned c = (unsigned)(valid ? c_raw : prm.ncols - 1);  // clamp: loads stay in bounds
+    const unsigned cq = c / (unsigned)prm.cpb;
+    const unsigned cr = c - cq * (unsigned)prm.cpb;
+    return {reinterpret_cast<cx<T>*>(prm.data) + ((long long)cq * prm.grp_stride + cr), cq, cr, valid};
+  };
+  auto prefetch = [&](const Col& col) {
+#pragma unroll
+    for (int kk = 0; kk < E; ++kk) cp_async<sizeof(cx<T>)>(pf + kk * NT + t, col.p + offset(tt + TPT * kk));
+    cp_commit();
+  };
 
-  cx<T> v[SH::E];
+  long long tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  Col cur = column(tile);
+  prefetch(cur);
+  for (; tile < ntiles; tile += gridDim.x) {
+    cx<T> v[E];
+    cp_wait_all();
 #pragma unroll
-  for (int u = 0; u < SH::E / SH::R0; ++u)
-#pragma unroll
-    for (int m = 0; m < SH::R0; ++m) v[u * SH::R0 + m] = col[offset(SH::in_elem(tt, u, m))];
+    for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = pf[kk * NT + t];
+    ST::first(v, tt, tw);  // consumes v: the slots are free for the next tile
+    const long long nxt = tile + gridDim.x;
+    Col next = cur;
+    if (nxt < ntiles) {
+      next = column(nxt);
+      prefetch(next);
+    }
+    ST::finish(xs, v, tt, b, tw);
 
-  ST::run(sm, v, tt, b, tw);
-
-  if (!valid) return;
-  if constexpr (REDIR) {
-    cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging) + ((long long)cq * prm.stg_grp + cr);
-    const unsigned bmask = (1u << prm.band_shift) - 1u;
-    const unsigned sb = (unsigned)prm.stg_band, sw = (unsigned)prm.stg_within;
+    if (cur.valid) {
+      if constexpr (REDIR) {
+        cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging) + ((long long)cur.cq * prm.stg_grp + cur.cr);
+        const unsigned bmask = (1u << prm.band_shift) - 1u;
+        const unsigned sb = (unsigned)prm.stg_band, sw = (unsigned)prm.stg_within;
 #pragma unroll
-    for (int u = 0; u < SH::E / SH::RL; ++u)
+        for (int u = 0; u < E / SH::RL; ++u)
 #pragma unroll
-      for (int m = 0; m < SH::RL; ++m) {
-        const unsigned e = SH::out_elem(tt, u, m);
-        const int band = (int)(e >> prm.band_shift);
-        if (band != prm.self_band) stg[band * sb + (e & bmask) * sw] = v[u * SH::RL + m];
-        else col[offset(e)] = v[u * SH::RL + m];
+          for (int m = 0; m < SH::RL; ++m) {
+            const unsigned e = SH::out_elem(tt, u, m);
+            const int band = (int)(e >> prm.band_shift);
+            if (band != prm.self_band) stg[band * sb + (e & bmask) * sw] = v[u * SH::RL + m];
+            else cur.p[offset(e)] = v[u * SH::RL + m];
+          }
+      } else {
+#pragma unroll
+        for (int u = 0; u < E / SH::RL; ++u)
+#pragma unroll
+          for (int m = 0; m < SH::RL; ++m) cur.p[offset(SH::out_elem(tt, u, m))] = v[u * SH::RL + m];
       }
-  } else {
-#pragma unroll
-    for (int u = 0; u < SH::E / SH::RL; ++u)
-#pragma unroll
-      for (int m = 0; m < SH::RL; ++m) col[offset(SH::out_elem(tt, u, m))] = v[u * SH::RL + m];
+    }
+    cur = next;
   }
 }
 

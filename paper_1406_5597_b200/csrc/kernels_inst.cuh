@@ -1,5 +1,7 @@
 // Explicit instantiation + runtime dispatch of the stage kernels for one
 // precision.  Included by kernels_f64.cu / kernels_f32.cu with TFFFT_REAL set.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace tffft {
@@ -10,6 +12,16 @@ static cudaError_t prep_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+static int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 template <typename T, int L, bool INV, bool TWO, bool REDIR>
 static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   using CF = ColCfg<T, L>;
@@ -17,8 +29,14 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   auto k = col_fft_kernel<T, L, INV, TWO, REDIR>;
   static cudaError_t prep = prep_smem(k, sm);
   if (prep != cudaSuccess) return prep;
-  const long long blocks = (p.ncols + CF::B - 1) / CF::B;
-  if (blocks <= 0) return cudaSuccess;
+  static int per_sm = [&] {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CF::THREADS, sm);
+    return n < 1 ? 1 : n;
+  }();
+  const long long tiles = (p.ncols + CF::B - 1) / CF::B;
+  if (tiles <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>(tiles, (long long)per_sm * num_sms());
   k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
   return cudaGetLastError();
 }
