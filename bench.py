@@ -1,0 +1,342 @@
+"""Benchmark: 3D r2c+c2r FFT pair (forward + inverse) on B200 through libtffft.
+
+Default workload (BASELINE.json headline): 1024^3 float64, slab-decomposed
+over the N GPUs of the job (strong scaling; p = N).  Prints ONE JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--grid 1024] [--dtype float64]
+  python bench.py --impl reference ...   # CPU oracle port of the reference path
+
+value  = GFLOP/s of the whole job, 2 * 2.5 N log2 N per pair, inputs resident in
+         HBM, device-timed (CUDA events, barrier + synchronize both sides, max
+         over ranks).  The inputs (8.6 GB/slab at p=1) are far larger than L2.
+e2e    = the same metric through the public API with host buffers: pinned-host
+         -> device copy of the real slab, forward, inverse, device -> host copy
+         of the result, all inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "3D r2c+c2r FFT pair: ms & GFLOP/s at 1/2/4/8 B200, % of HBM/NVLink roofline"
+HBM_FALLBACK = 6650.0   # GB/s, B200_PROFILING.md fallback
+NVLINK_GBS = 770.0      # measured peer copy per direction (B200_PROFILING.md)
+
+
+def pair_flops(n0, n1, n2):
+    n = n0 * n1 * n2
+    return 2 * 2.5 * n * math.log2(n)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def algorithmic_bytes(n0, n1, n2, p, s_r):
+    """HBM bytes per GPU per pair, NVLink bytes per GPU per pair,
+    and the bytes of one stage-3 launch (read + write of the spectral slab)."""
+    n, nc = n0 * n1 * n2, n0 * n1 * (n2 // 2 + 1)
+    s_c = 2 * s_r
+    hbm = 2 * (s_r * n + 3 * s_c * nc) / p
+    nvl = 2 * s_c * nc * (p - 1) / (p * p)
+    stage3 = 2 * s_c * nc / p
+    return hbm, nvl, stage3
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return None
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference path port): bounded sample of the same workload
+# ---------------------------------------------------------------------------
+
+def cpu_sample(n0, n1, n2, planes=8, workers=None):
+    """Time the oracle (restatement of the reference's STRIDED pipeline,
+    bit-identical to it) on a bounded sample of the full-size workload and
+    extrapolate: stage 1 + 1' on `planes` of the n0 planes, stage 3 + 3' on
+    the same fraction of the n1*n2c columns (gather -> c2c -> scatter)."""
+    import numpy as np
+
+    import oracle
+
+    workers = workers or len(os.sched_getaffinity(0))
+    n2c = n2 // 2 + 1
+    rng = np.random.default_rng(0)
+    slab = rng.uniform(-1.0, 1.0, size=(planes, n1, n2))
+    ncols = max(1, (n1 * n2c * planes) // n0)
+    t0 = time.perf_counter()
+    spec = oracle.stage1_forward(slab, workers)
+    oracle.stage1_inverse(spec, n2, workers)
+    t1 = time.perf_counter()
+    # stage 3 on ncols columns of length n0 laid out (n0, ncols): same gather/scatter pattern
+    flat = (rng.standard_normal((n0, ncols)) + 1j * rng.standard_normal((n0, ncols))).reshape(-1)
+    offs = (np.arange(n0)[None, :] * ncols + np.arange(ncols)[:, None])
+    for inv in (False, True):
+        def work(a, b, inv=inv):
+            cols = flat[offs[a:b]]
+            oracle.c2c_rows(cols, inv)
+            flat[offs[a:b]] = cols
+        oracle.slabfft_oracle._run(work, oracle.slabfft_oracle._chunks(ncols, workers), workers)
+    t2 = time.perf_counter()
+    scale1 = n0 / planes
+    scale3 = (n1 * n2c) / ncols
+    t_full = (t1 - t0) * scale1 + (t2 - t1) * scale3
+    sample = (f"oracle port, {workers} threads: stage 1+1' on {planes}/{n0} planes and stage 3+3' on "
+              f"{ncols}/{n1 * n2c} columns of the {n0}x{n1}x{n2} float64 pair, extrapolated "
+              f"({t2 - t0:.1f} s measured)")
+    return pair_flops(n0, n1, n2) / t_full / 1e9, t_full, workers, sample
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n0 = n1 = n2 = args.grid
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gf, t_full, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
+        if i >= args.warmup:
+            vals.append((gf, t_full))
+    gf = statistics.median(v[0] for v in vals)
+    ms = statistics.median(v[1] for v in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{n0}x{n1}x{n2} float64 r2c+c2r pair", "grid": [n0, n1, n2], "p": 1},
+        "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1406_5597_b200 as tf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        ep = tf.init_nccl_endpoint(local)
+    else:
+        ep = tf.make_communicators(1, device=local)[0]
+    p = world
+    n0 = n1 = n2 = args.grid
+    grid = tf.GlobalGrid(n0, n1, n2)
+    dt = args.dtype
+    s_r = 8 if dt == "float64" else 4
+    fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dt, check_consistency=False)
+    rdt = tf.DTYPES[dt][1]
+    n0p = n0 // p
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    x = torch.empty(n0p * n1 * n2, dtype=rdt, device=dev)
+    x.uniform_(-1.0, 1.0, generator=gen)
+    slab = tf.RealSlab(fp.real_layout, x)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # correctness guard on the timed configuration (reference cli.py:263-271 style)
+    tf.inverse(fp, tf.forward(fp, slab))
+    torch.cuda.synchronize(dev)
+    rt = (torch.linalg.norm(fp.real_out.double() - x.double()) / torch.linalg.norm(x.double())).item()
+    tol = 1e-12 if dt == "float64" else 1e-5
+    if not rt <= tol:
+        raise SystemExit(f"round-trip check failed: rel L2 {rt:.3e} > {tol}")
+
+    for _ in range(args.warmup):
+        tf.inverse(fp, tf.forward(fp, slab))
+    barrier()
+    fp.enable_timing(True)
+    fp.reset_instrumentation()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            tf.inverse(fp, tf.forward(fp, slab))
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = fp.launches
+    stages = fp.timers_us
+    fp.enable_timing(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # e2e through the public API with host buffers
+    h_in = torch.empty(n0p * n1 * n2, dtype=rdt, pin_memory=True)
+    h_in.copy_(x)
+    h_out = torch.empty_like(h_in, pin_memory=True)
+    d_in = torch.empty_like(x)
+    barrier()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    tf.inverse(fp, tf.forward(fp, slab))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d_in.copy_(h_in, non_blocking=True)
+        back = tf.inverse(fp, tf.forward(fp, tf.RealSlab(fp.real_layout, d_in)))
+        h_out.copy_(back.data, non_blocking=True)
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    flops = pair_flops(n0, n1, n2)
+    value = flops / (ms * 1e-3) / 1e9
+    hbm_peak, peak_kind = peaks()
+    hbm, nvl, st3 = algorithmic_bytes(n0, n1, n2, p, s_r)
+    t_roof = max(hbm / (hbm_peak * 1e9), nvl / (NVLINK_GBS * 1e9) if p > 1 else 0.0) * 1e3
+    # dominant kernel: the stage-3 strided column c2c (one launch per direction)
+    st3_ms = stages["stage3_us"] / 1e3 / (2 * args.steps)
+    st1_ms = stages["stage1_us"] / 1e3 / (2 * args.steps)
+    ach = st3 / (st3_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "stage3_traffic.json")
+    try:
+        with open(tpath) as f:
+            tr = json.load(f)
+        key = f"{n0}x{n1}x{n2}_{dt}_p{p}"
+        traffic = tr.get(key)
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if dt == "float64" else "f32",
+        "data": "synthetic: seeded uniform[-1,1) real field generated on device",
+        "config": {
+            "workload": f"{n0}x{n1}x{n2} {dt} r2c+c2r pair, slab p={p}",
+            "grid": [n0, n1, n2], "p": p, "parallelism": f"slab{p}",
+            "l2": f"inputs larger than L2 ({n0p * n1 * n2 * s_r / 1e9:.2f} GB real slab per GPU)",
+            "pair_roofline_ms": t_roof, "pair_roofline_frac": t_roof / ms,
+            "stage_ms": {"stage1+1'": st1_ms * 2, "exchange": stages["exchange_us"] / 1e3 / args.steps,
+                         "stage3+3'": st3_ms * 2},
+            "roundtrip_rel_l2": rt,
+        },
+        "roofline": {"bound": "hbm", "kernel": "col_fft_kernel (stage 3 strided n0 c2c)",
+                     "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": ach / hbm_peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": st3},
+        "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h_in.numel() * h_in.element_size(),
+                "d2h_bytes_per_step": h_out.numel() * h_out.element_size()},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gf, _, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
+        line["cpu_baseline"] = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line))
+    fp.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--grid", type=int, default=1024)
+    ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-planes", type=int, default=32)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -12,7 +12,7 @@ import threading
 
 from .errors import STATUS_TO_ERROR, SlabFftError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtffft.so")
+LIB_PATH = os.environ.get("TFFFT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtffft.so")
 
 # name -> (restype, argtypes)
 _c = ctypes

@@ -30,6 +30,10 @@ struct ColParams {
   long long inner_stride, block_stride;
   int band_shift, self_band;
   long long stg_band, stg_within, stg_grp;
+  // L2 prefetch of wide row segments for the tile `pf_ahead` tiles ahead
+  // (0 = off): DRAM then sees pf_bytes-wide row visits instead of B*sizeof(cx)
+  long long pf_ahead;
+  int pf_bytes;
 };
 
 // Rows: row r of real data at real + r*n2 (reals); complex row at spec + r*n2c.
@@ -51,17 +55,28 @@ struct RowParams {
 // its complex values into two rounds).  X layout: one pad word per E words
 // inside a column, column stride S == 4 mod 16 words, so the 16 lanes of an
 // 8-byte LDS/STS wavefront (4 columns x 4 threads) hit 16 distinct bank pairs.
+#ifndef TFFFT_COLB
+#define TFFFT_COLB 8
+#endif
+#ifndef TFFFT_SPLIT
+#define TFFFT_SPLIT 1
+#endif
+#ifndef TFFFT_PREFETCH
+#define TFFFT_PREFETCH 1
+#endif
 template <typename T, int L> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
-  static constexpr int B = L >= 12 ? 2 : (256 / TPT > 4 ? 256 / TPT : 4);
+  static constexpr int B = L >= 12 ? 2 : (256 / TPT > TFFFT_COLB ? 256 / TPT : (TPT * TFFFT_COLB > 1024 ? 1024 / TPT : TFFFT_COLB));
   static constexpr int THREADS = TPT * B;
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
   static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
-  static constexpr int S = ((RAW + 15) / 16) * 16 + 4;
-  static constexpr bool SPLIT = sizeof(T) == 8;
+  static constexpr bool SPLIT = sizeof(T) == 8 && TFFFT_SPLIT;
+  static constexpr int WORD = SPLIT ? 8 : (int)sizeof(cx<T>);  // exchange word bytes
+  static constexpr int QW = 128 / WORD;                          // words per 128 bytes
+  static constexpr int S = ((RAW + QW - 1) / QW) * QW + QW / 4;
   static constexpr bool XCHG = Shape<L>::P > 1;
-  static constexpr size_t P_BYTES = sizeof(cx<T>) * THREADS * Shape<L>::E;
-  static constexpr size_t X_BYTES = XCHG ? 8 * (size_t)B * S : 0;
+  static constexpr size_t P_BYTES = TFFFT_PREFETCH ? sizeof(cx<T>) * THREADS * Shape<L>::E : 0;
+  static constexpr size_t X_BYTES = XCHG ? (size_t)WORD * B * S : 0;
 };
 
 template <int L> struct RowCfg {
@@ -137,18 +152,39 @@ col_fft_kernel(const ColParams prm) {
   long long tile = blockIdx.x;
   if (tile >= ntiles) return;
   Col cur = column(tile);
-  prefetch(cur);
+  if (TFFFT_PREFETCH) prefetch(cur);
+  // tiles sharing one pf_bytes-wide row segment; each prefetches N/GT rows
+  const int GT = prm.pf_ahead > 0 ? prm.pf_bytes / (B * (int)sizeof(cx<T>)) : 1;
   for (; tile < ntiles; tile += gridDim.x) {
+    if (prm.pf_ahead > 0) {
+      const long long tp = tile + prm.pf_ahead;
+      const int rows = SH::N / GT;
+      if (tp < ntiles && t < rows) {
+        const long long c0 = (tp / GT) * GT * B;
+        if (c0 + (long long)GT * B <= prm.ncols) {
+          const unsigned e = (unsigned)((tp % GT) * rows + t);
+          const cx<T>* p = reinterpret_cast<const cx<T>*>(prm.data) + c0 + offset(e);
+          prefetch_l2(p, (unsigned)prm.pf_bytes);
+        }
+      }
+    }
     cx<T> v[E];
-    cp_wait_all();
-#pragma unroll
-    for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = pf[kk * NT + t];
-    ST::first(v, tt, tw);  // consumes v: the slots are free for the next tile
-    const long long nxt = tile + gridDim.x;
     Col next = cur;
-    if (nxt < ntiles) {
-      next = column(nxt);
-      prefetch(next);
+    const long long nxt = tile + gridDim.x;
+    if (TFFFT_PREFETCH) {
+      cp_wait_all();
+#pragma unroll
+      for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = pf[kk * NT + t];
+      ST::first(v, tt, tw);  // consumes v: the slots are free for the next tile
+      if (nxt < ntiles) {
+        next = column(nxt);
+        prefetch(next);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = cur.p[offset(tt + TPT * kk)];
+      ST::first(v, tt, tw);
+      if (nxt < ntiles) next = column(nxt);
     }
     ST::finish(xs, v, tt, b, tw);
 

@@ -36,7 +36,11 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   }();
   const long long tiles = (p.ncols + CF::B - 1) / CF::B;
   if (tiles <= 0) return cudaSuccess;
+#ifdef TFFFT_NONPERSISTENT
+  const long long blocks = tiles;
+#else
   const long long blocks = std::min<long long>(tiles, (long long)per_sm * num_sms());
+#endif
   k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
   return cudaGetLastError();
 }

@@ -332,6 +332,17 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   c.band_shift = ilog2(pl->n0p);
   c.self_band = pl->rank;
   c.staging = nullptr;
+  // stage 3 walks rows n1*n2c elements apart: widen the DRAM row visits with
+  // L2 prefetches one resident wave ahead (tools/micro/stride_bw2.cu)
+  {
+    static const char* env = getenv("TFFFT_L2PF");
+    const long long ahead = env ? atoll(env) : 0;
+    const int pfb = 256;
+    const bool aligned = ((long long)pl->n1p * pl->n2c * (long long)pl->esz) % pfb == 0 &&
+                         ((long long)pl->n1 * pl->n2c * (long long)pl->esz) % pfb == 0;
+    c.pf_ahead = aligned ? ahead : 0;
+    c.pf_bytes = pfb;
+  }
   if (inv && pl->p > 1) {
     // inverse epilogue: block s != rank -> staging[s][i][c]
     c.staging = pl->staging;
