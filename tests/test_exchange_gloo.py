@@ -1,0 +1,69 @@
+"""Multi-rank host path on CPU (gloo, world_size 2 and 4): each rank takes
+the oracle's stage-1 output, splits it the way the GPU stage-1 epilogue does
+(self band in place, peer bands to staging[q][i]), executes libtffft's
+exchange schedule with torch.distributed send/recv, runs the oracle's
+stage 3 and must land bit-exactly on the reference's forward output."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, shape, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1406_5597_b200 as tf
+
+        n0, n1, n2 = shape
+        x = oracle.normal_field(shape, 11)
+        n0p = n0 // world
+        s1 = oracle.stage1_forward(x[rank * n0p:(rank + 1) * n0p])
+        spec, staging = oracle.stage1_band_staging(s1, world, rank)
+        flat = torch.from_numpy(spec.reshape(-1).copy())
+        stg = torch.from_numpy(staging.reshape(-1).copy())
+        ops = tf.exchange_schedule(n0, n1, n2, world, rank)
+        reqs = []
+        for op in ops:  # libtffft posts all sends and receives of a rank in one group
+            reqs.append(dist.isend(stg[op.send_offset:op.send_offset + op.count].clone(), op.peer))
+        for op in ops:
+            reqs.append(dist.irecv(flat[op.recv_offset:op.recv_offset + op.count], op.peer))
+        for r in reqs:
+            r.wait()
+        out = flat.numpy().copy()
+        oracle.stage3(out, n0, n1, n2, world, inverse=False)
+        ref = oracle.forward_all(x, world)[rank]
+        q.put((rank, bool(np.array_equal(out.view(np.float64), ref.view(np.float64)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (8, 8, 8)), (2, (16, 4, 32)), (4, (8, 16, 4))])
+def test_exchange_schedule_over_gloo(world, shape):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res

@@ -1,0 +1,118 @@
+"""The C-ABI library: loads without a GPU, exports every symbol
+include/tffft.h declares, and its host-only entry points (exchange
+schedule, radix schedule, communicator bookkeeping, argument checking)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1406_5597_b200 as tf
+from paper_1406_5597_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "tffft.h")).read()
+    return sorted(set(re.findall(r"\b(tffft_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.SYMBOLS)
+
+
+def test_version():
+    assert _lib.lib().tffft_version() >= 100
+
+
+def test_radix_schedule_matches_design():
+    lib = _lib.lib()
+    got = {}
+    for L in range(0, 13):
+        r = (ctypes.c_int * 8)()
+        n = ctypes.c_int()
+        _lib.check(lib.tffft_radix_schedule(L, r, ctypes.byref(n)))
+        got[L] = [r[i] for i in range(n.value)]
+        prod = 1
+        for x in got[L]:
+            prod *= x
+            assert x <= 16
+        assert prod == 1 << L
+    assert got[10] == [16, 8, 8] and got[9] == [8, 8, 8] and got[11] == [16, 16, 8]
+
+
+@pytest.mark.parametrize("n0,n1,n2,p", [(4, 4, 2, 2), (8, 8, 8, 4), (16, 8, 32, 8), (128, 128, 128, 2)])
+def test_exchange_schedule_geometry(n0, n1, n2, p):
+    """Each op is one block of the reference's STRIDED LayoutDescriptor
+    (exchange.py:114-119); send and receive cover every off-rank element once."""
+    n0p, n1p, n2c = n0 // p, n1 // p, n2 // 2 + 1
+    for rank in range(p):
+        ops = tf.exchange_schedule(n0, n1, n2, p, rank)
+        assert len(ops) == (p - 1) * n0p
+        recv = set()
+        for op in ops:
+            assert op.peer != rank and op.count == n1p * n2c
+            q, i = op.peer, (op.recv_offset // (n1 * n2c))
+            assert op.recv_offset == i * n1 * n2c + q * n1p * n2c
+            assert op.send_offset == (q * n0p + i) * n1p * n2c
+            recv.update(range(op.recv_offset, op.recv_offset + op.count))
+        # every element outside the self band is received exactly once
+        want = {i * n1 * n2c + q * n1p * n2c + c for i in range(n0p) for q in range(p) if q != rank
+                for c in range(n1p * n2c)}
+        assert recv == want
+
+
+def test_exchange_schedule_rejects_bad_geometry():
+    with pytest.raises(tf.ConfigurationError):
+        tf.exchange_schedule(6, 8, 8, 4, 0)
+
+
+def test_local_communicators_host_bookkeeping():
+    lib = _lib.lib()
+    arr = (ctypes.c_void_p * 3)()
+    _lib.check(lib.tffft_comm_init_local(3, 0, arr))
+    for r in range(3):
+        v = ctypes.c_int()
+        _lib.check(lib.tffft_comm_rank(arr[r], ctypes.byref(v)))
+        assert v.value == r
+        _lib.check(lib.tffft_comm_size(arr[r], ctypes.byref(v)))
+        assert v.value == 3
+    _lib.check(lib.tffft_comm_abort(arr[0]))
+    for r in range(3):
+        _lib.check(lib.tffft_comm_destroy(arr[r]))
+
+
+def test_plan_create_validates_before_touching_the_gpu():
+    lib = _lib.lib()
+    arr = (ctypes.c_void_p * 2)()
+    _lib.check(lib.tffft_comm_init_local(2, 0, arr))
+    h = ctypes.c_void_p()
+    cases = [((6, 8, 8), tf.ConfigurationError),   # not a power of two
+             ((8, 8, 1), tf.ConfigurationError),   # axis < 2
+             ((8, 8, 8192), tf.SizeError),         # beyond the kernels' 4096 limit
+             ((8, 6, 8), tf.ConfigurationError)]
+    for (n0, n1, n2), err in cases:
+        with pytest.raises(err):
+            _lib.check(lib.tffft_plan_create(n0, n1, n2, 0, 0, arr[0], ctypes.byref(h)))
+    with pytest.raises(tf.ConfigurationError):  # unknown dtype
+        _lib.check(lib.tffft_plan_create(8, 8, 8, 7, 0, arr[0], ctypes.byref(h)))
+    with pytest.raises(tf.ConfigurationError):  # COLLECTIVE pattern not on the GPU path
+        _lib.check(lib.tffft_plan_create(8, 8, 8, 0, 1, arr[0], ctypes.byref(h)))
+    for r in range(2):
+        lib.tffft_comm_destroy(arr[r])
+
+
+def test_status_codes_map_to_reference_exceptions():
+    from paper_1406_5597_b200.errors import STATUS_TO_ERROR
+    assert STATUS_TO_ERROR[1] is tf.SizeError
+    assert STATUS_TO_ERROR[3] is tf.ConfigurationError
+    assert STATUS_TO_ERROR[4] is tf.ContractError
+    assert STATUS_TO_ERROR[7] is tf.ConsistencyError
+    assert issubclass(tf.ConfigurationError, ValueError) and issubclass(tf.ContractError, tf.SlabFftError)
