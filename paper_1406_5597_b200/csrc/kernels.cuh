@@ -53,8 +53,8 @@ struct RowParams {
 // thread.  Shared memory = the prefetch slots P (THREADS*E complex, each
 // thread's own slots) + the exchange buffer X in 8-byte words (float64 splits
 // its complex values into two rounds).  X layout: one pad word per E words
-// inside a column, column stride S == 4 mod 16 words, so the 16 lanes of an
-// 8-byte LDS/STS wavefront (4 columns x 4 threads) hit 16 distinct bank pairs.
+// inside a column, column stride S == 16/B mod 16 words, so the 16 lanes of an
+// 8-byte LDS/STS wavefront (B columns x 16/B threads) hit 16 distinct bank pairs.
 #ifndef TFFFT_COLB
 #define TFFFT_COLB 8
 #endif
@@ -64,16 +64,27 @@ struct RowParams {
 #ifndef TFFFT_PREFETCH
 #define TFFFT_PREFETCH 1
 #endif
+// columns per CTA: at least 256 threads, at most 1024 threads and 227 KB of
+// shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
+template <typename T, int L>
+__host__ __device__ constexpr int col_batch() {
+  constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
+  int b = 256 / TPT > TFFFT_COLB ? 256 / TPT : TFFFT_COLB;
+  while (b > 1 && (TPT * b > 1024 || (size_t)b * N * (sizeof(cx<T>) + 8) + 4096 > 227 * 1024)) b /= 2;
+  return b;
+}
 template <typename T, int L> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
-  static constexpr int B = L >= 12 ? 2 : (256 / TPT > TFFFT_COLB ? 256 / TPT : (TPT * TFFFT_COLB > 1024 ? 1024 / TPT : TFFFT_COLB));
+  static constexpr int B = col_batch<T, L>();
   static constexpr int THREADS = TPT * B;
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
   static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
   static constexpr bool SPLIT = sizeof(T) == 8 && TFFFT_SPLIT;
   static constexpr int WORD = SPLIT ? 8 : (int)sizeof(cx<T>);  // exchange word bytes
   static constexpr int QW = 128 / WORD;                          // words per 128 bytes
-  static constexpr int S = ((RAW + QW - 1) / QW) * QW + QW / 4;
+  // B columns x (QW/B) consecutive threads share one wavefront: offset column b
+  // by b*QW/B words so the wavefront covers every bank exactly once
+  static constexpr int S = ((RAW + QW - 1) / QW) * QW + (QW / B > 0 ? QW / B : 1);
   static constexpr bool XCHG = Shape<L>::P > 1;
   static constexpr size_t P_BYTES = TFFFT_PREFETCH ? sizeof(cx<T>) * THREADS * Shape<L>::E : 0;
   static constexpr size_t X_BYTES = XCHG ? (size_t)WORD * B * S : 0;

@@ -41,6 +41,7 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
 #else
   const long long blocks = std::min<long long>(tiles, (long long)per_sm * num_sms());
 #endif
+  (void)cudaGetLastError();  // clear any stale error of this thread
   k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
   return cudaGetLastError();
 }
@@ -54,6 +55,7 @@ static cudaError_t r2c_one(const RowParams& p, cudaStream_t s) {
   if (prep != cudaSuccess) return prep;
   const long long blocks = (p.nrows + RC::B - 1) / RC::B;
   if (blocks <= 0) return cudaSuccess;
+  (void)cudaGetLastError();  // clear any stale error of this thread
   k<<<(unsigned)blocks, RC::THREADS, sm, s>>>(p);
   return cudaGetLastError();
 }
@@ -67,6 +69,7 @@ static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
   if (prep != cudaSuccess) return prep;
   const long long blocks = (p.nrows + RC::B - 1) / RC::B;
   if (blocks <= 0) return cudaSuccess;
+  (void)cudaGetLastError();  // clear any stale error of this thread
   k<<<(unsigned)blocks, RC::THREADS, sm, s>>>(p);
   return cudaGetLastError();
 }
