@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "fourstep.cuh"
 
 namespace tffft {
 
@@ -125,6 +126,45 @@ cudaError_t launch_c2r_rows<TFFFT_REAL>(int L, const RowParams& p, cudaStream_t 
     TFFFT_ROW_CASE(3, c2r_one) TFFFT_ROW_CASE(4, c2r_one) TFFFT_ROW_CASE(5, c2r_one)
     TFFFT_ROW_CASE(6, c2r_one) TFFFT_ROW_CASE(7, c2r_one) TFFFT_ROW_CASE(8, c2r_one)
     TFFFT_ROW_CASE(9, c2r_one) TFFFT_ROW_CASE(10, c2r_one) TFFFT_ROW_CASE(11, c2r_one)
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int LA, int LB, bool INV, bool TWO, bool REDIR>
+static cudaError_t fs_one(const FourStepParams& p, cudaStream_t s) {
+  const size_t sm = fourstep_smem_bytes<T, LA, LB>();
+  auto k = fourstep_kernel<T, LA, LB, INV, TWO, REDIR>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  static int per_sm = [&] {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFsThreads, sm);
+    return n < 1 ? 1 : n;
+  }();
+  (void)cudaGetLastError();
+  k<<<(unsigned)(per_sm * num_sms()), kFsThreads, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int LA, int LB>
+static cudaError_t fs_dispatch(bool inv, int variant, const FourStepParams& p, cudaStream_t s) {
+  if (!inv) {
+    if (variant == 0) return fs_one<T, LA, LB, false, false, false>(p, s);
+    if (variant == 2) return fs_one<T, LA, LB, false, true, false>(p, s);
+  } else {
+    if (variant == 0) return fs_one<T, LA, LB, true, false, false>(p, s);
+    if (variant == 3) return fs_one<T, LA, LB, true, true, true>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t launch_fourstep<TFFFT_REAL>(int L, bool inv, int variant, const FourStepParams& p, cudaStream_t s) {
+  switch (L) {
+    case 9: return fs_dispatch<TFFFT_REAL, 5, 4>(inv, variant, p, s);
+    case 10: return fs_dispatch<TFFFT_REAL, 5, 5>(inv, variant, p, s);
+    case 11: return fs_dispatch<TFFFT_REAL, 6, 5>(inv, variant, p, s);
+    case 12: return fs_dispatch<TFFFT_REAL, 6, 6>(inv, variant, p, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/tffft.h"
+#include "fourstep.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 
@@ -201,6 +202,13 @@ struct tffft_plan_s {
   void* tw2post = nullptr;
   unsigned long long* stats = nullptr;
   void** pull_ptrs = nullptr;  // local fabric: device array [2 * nchunks] of (src, dst)
+  // stage-3 four-step (fourstep.cuh): L2-resident scratch ring, counters, tables
+  int fs_la = 0, fs_G = 0, fs_groups = 0;
+  void* fs_scratch = nullptr;
+  unsigned* fs_counters = nullptr;
+  void* fs_twA = nullptr;
+  void* fs_twB = nullptr;
+  void* fs_twN = nullptr;
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -227,6 +235,17 @@ static std::vector<double> pass_table(int L) {
       t[2 * (off + k)] = (double)cosl(a);
       t[2 * (off + k) + 1] = (double)sinl(a);
     }
+  }
+  return t;
+}
+
+// exp(-2 pi i t / n) for t < n (four-step twiddles)
+static std::vector<double> full_table(int n) {
+  std::vector<double> t(2 * (size_t)n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    const long double a = -2.0L * 3.141592653589793238462643383279502884L * k / (long double)n;
+    t[2 * k] = (double)cosl(a);
+    t[2 * k + 1] = (double)sinl(a);
   }
   return t;
 }
@@ -318,8 +337,37 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   return TFFFT_OK;
 }
 
+static cudaError_t fs_launch(tffft_plan_t pl, bool inv, int variant, const FourStepParams& prm, cudaStream_t s) {
+  pl->launches++;
+  return pl->dtype == TFFFT_F64 ? launch_fourstep<double>(pl->L0, inv, variant, prm, s)
+                                : launch_fourstep<float>(pl->L0, inv, variant, prm, s);
+}
+
 // stage 3 / 3': c2c along n0 of every STRIDED_INPLACE column c = j*n2c + k
 static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  if (pl->fs_la > 0) {
+    FourStepParams f{};
+    f.data = spec;
+    f.staging = (inv && pl->p > 1) ? pl->staging : nullptr;
+    f.scratch = pl->fs_scratch;
+    f.twA = pl->fs_twA;
+    f.twB = pl->fs_twB;
+    f.twN = pl->fs_twN;
+    f.counters = pl->fs_counters;
+    f.ncols = (long long)pl->n1p * pl->n2c;
+    f.G = pl->fs_G;
+    f.ngroups = pl->fs_groups;
+    f.ic_shift = ilog2(pl->n0p);
+    f.inner_stride = (long long)pl->n1 * pl->n2c;
+    f.block_stride = (long long)pl->n1p * pl->n2c;
+    f.band_shift = ilog2(pl->n0p);
+    f.self_band = pl->rank;
+    f.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
+    f.stg_within = (long long)pl->n1p * pl->n2c;
+    CUDA_TRY(cudaMemsetAsync(pl->fs_counters, 0, sizeof(unsigned) * (1 + 2 * (size_t)pl->fs_groups), s));
+    CUDA_TRY(fs_launch(pl, inv, pl->p == 1 ? 0 : (f.staging ? 3 : 2), f, s));
+    return TFFFT_OK;
+  }
   ColParams c{};
   c.data = spec;
   c.tw = pl->tw0;
@@ -597,6 +645,28 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
       TRY(fabric_setup(pl.get(), nullptr));
     }
   }
+  // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
+  {
+    static const char* env_off = getenv("TFFFT_NO_FOURSTEP");
+    const int la = env_off ? 0 : fourstep_la(pl->L0);
+    if (la > 0) {
+      static const char* env_g = getenv("TFFFT_FS_G");
+      const long long ncols = (long long)pl->n1p * pl->n2c;
+      long long G = env_g ? atoll(env_g) : 1024;
+      G = std::max<long long>(kFsMaxW, (G / kFsMaxW) * kFsMaxW);
+      G = std::min<long long>(G, ((ncols + kFsMaxW - 1) / kFsMaxW) * kFsMaxW);
+      pl->fs_la = la;
+      pl->fs_G = (int)G;
+      pl->fs_groups = (int)((ncols + G - 1) / G);
+      const size_t sb = (size_t)kFsSlots * n0 * G * pl->esz;
+      CUDA_TRY(cudaMalloc(&pl->fs_scratch, sb));
+      CUDA_TRY(cudaMalloc(&pl->fs_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->fs_groups)));
+      ws += sb + sizeof(unsigned) * (1 + 2 * (size_t)pl->fs_groups);
+      TRY(upload_table(pass_table(la), dtype, &pl->fs_twA, &ws));
+      TRY(upload_table(pass_table(pl->L0 - la), dtype, &pl->fs_twB, &ws));
+      TRY(upload_table(full_table(n0), dtype, &pl->fs_twN, &ws));
+    }
+  }
   pl->workspace = ws;
   *out = pl.release();
   return TFFFT_OK;
@@ -627,6 +697,8 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   free_events(pl);
   cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
   cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->pull_ptrs);
+  cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
+  cudaFree(pl->fs_twN);
   delete pl;
   return TFFFT_OK;
 }
