@@ -73,12 +73,41 @@ __device__ __forceinline__ cx<T> ldcg_cx(const cx<T>* p) {
   auto v = __ldcg(reinterpret_cast<const typename vec2<T>::type*>(p));
   return {v.x, v.y};
 }
-template <typename T>
-__device__ __forceinline__ void stcg_cx(cx<T>* p, cx<T> z) {
-  typename vec2<T>::type v;
-  v.x = z.x;
-  v.y = z.y;
-  __stcg(reinterpret_cast<typename vec2<T>::type*>(p), v);
+// L2 eviction-priority policies: HBM streaming data evict_first, the scratch
+// ring evict_last (it must survive from pass A to pass B)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ cx<double> ld_hint(const cx<double>* a, uint64_t pol) {
+  cx<double> z;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(z.x), "=d"(z.y) : "l"(a), "l"(pol));
+  return z;
+}
+__device__ __forceinline__ cx<float> ld_hint(const cx<float>* a, uint64_t pol) {
+  cx<float> z;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(z.x), "=f"(z.y) : "l"(a), "l"(pol));
+  return z;
+}
+__device__ __forceinline__ void st_hint(cx<double>* a, cx<double> z, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(z.x), "d"(z.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(cx<float>* a, cx<float> z, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(a), "f"(z.x), "f"(z.y), "l"(pol)
+               : "memory");
+}
+// drop an L2 line without writing it back (its scratch contents are consumed)
+__device__ __forceinline__ void discard_l2(const void* a) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
 }
 
 template <typename T, int LA, int LB, bool INV, bool TWO, bool REDIR>
@@ -92,7 +121,7 @@ fourstep_kernel(const FourStepParams prm) {
   using STA = Stockham<T, LA, INV, PA::S, PA::PS, PA::SPLIT>;
   using STB = Stockham<T, LB, INV, PB::S, PB::PS, PB::SPLIT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_task;
+  __shared__ int s_isA, s_g, s_w, s_end;
 
   const int t = threadIdx.x;
   cx<T>* data = reinterpret_cast<cx<T>*>(prm.data);
@@ -107,37 +136,48 @@ fourstep_kernel(const FourStepParams prm) {
   const int ng = prm.ngroups;
   const int blocksA = prm.G / PA::W, blocksB = prm.G / PB::W;
   const int nA = NB * blocksA, nB = NA * blocksB;
-  const long long total = (long long)ng * (nA + nB);
+  const unsigned total = (unsigned)ng * (unsigned)(nA + nB);
   unsigned* ticket = prm.counters;
   unsigned* doneA = prm.counters + 1;
   unsigned* doneB = prm.counters + 1 + ng;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
 
+  // thread 0 owns the queue: it always holds the NEXT ticket, fetched while the
+  // CTA works on the current task, so the atomic's round trip is hidden
+  unsigned next_tk = 0;
+  if (t == 0) next_tk = atomicAdd(ticket, 1u);
   for (;;) {
-    if (t == 0) s_task = (int)atomicAdd(ticket, 1u);
-    __syncthreads();
-    const long long tk = s_task;
-    if (tk >= total) break;
-    // decode: A(0), [A(q+1), B(q)] for q < ng-1, B(ng-1)
-    bool isA;
-    int g, w;
-    if (tk < nA) {
-      isA = true; g = 0; w = (int)tk;
-    } else {
-      const long long r = tk - nA;
-      const int q = (int)(r / (nA + nB));
-      const int x = (int)(r % (nA + nB));
-      if (q < ng - 1 && x < nA) { isA = true; g = q + 1; w = x; }
-      else { isA = false; g = q; w = q < ng - 1 ? x - nA : x; }
-    }
     if (t == 0) {
-      if (isA) {
-        if (g >= kFsSlots)
-          while (ld_acquire(doneB + (g - kFsSlots)) < (unsigned)nB) __nanosleep(128);
+      const unsigned tk = next_tk;
+      if (tk >= total) {
+        s_end = 1;
       } else {
-        while (ld_acquire(doneA + g) < (unsigned)nA) __nanosleep(128);
+        // decode: A(0), [A(q+1), B(q)] for q < ng-1, B(ng-1)
+        int isA, g, w;
+        if (tk < (unsigned)nA) {
+          isA = 1; g = 0; w = (int)tk;
+        } else {
+          const unsigned r = tk - (unsigned)nA;
+          const int q = (int)(r / (unsigned)(nA + nB));
+          const int x = (int)(r % (unsigned)(nA + nB));
+          if (q < ng - 1 && x < nA) { isA = 1; g = q + 1; w = x; }
+          else { isA = 0; g = q; w = q < ng - 1 ? x - nA : x; }
+        }
+        if (isA) {
+          if (g >= kFsSlots)
+            while (ld_acquire(doneB + (g - kFsSlots)) < (unsigned)nB) __nanosleep(64);
+        } else {
+          while (ld_acquire(doneA + g) < (unsigned)nA) __nanosleep(64);
+        }
+        s_end = 0; s_isA = isA; s_g = g; s_w = w;
+        next_tk = atomicAdd(ticket, 1u);
       }
     }
     __syncthreads();
+    if (s_end) break;
+    const bool isA = s_isA;
+    const int g = s_g, w = s_w;
     cx<T>* gscr = scr + (size_t)(g % kFsSlots) * N * prm.G;
     if (isA) {
       constexpr int W = PA::W;
@@ -151,7 +191,7 @@ fourstep_kernel(const FourStepParams prm) {
       for (int u = 0; u < SA::E / SA::R0; ++u)
 #pragma unroll
         for (int m = 0; m < SA::R0; ++m)
-          v[u * SA::R0 + m] = data[c + offset((unsigned)(NB * SA::in_elem(tt, u, m) + beta))];
+          v[u * SA::R0 + m] = ld_hint(data + c + offset((unsigned)(NB * SA::in_elem(tt, u, m) + beta)), pol_stream);
       STA::run(smem_raw, v, tt, b, reinterpret_cast<const cx<T>*>(prm.twA));
 #pragma unroll
       for (int u = 0; u < SA::E / SA::RL; ++u)
@@ -159,7 +199,7 @@ fourstep_kernel(const FourStepParams prm) {
         for (int m = 0; m < SA::RL; ++m) {
           const int alpha = SA::out_elem(tt, u, m);
           const cx<T> z = ctw<INV>(v[u * SA::RL + m], ldg_cx(twN + ((beta * alpha) & (N - 1))));
-          stcg_cx(gscr + ((size_t)alpha * NB + beta) * prm.G + lc, z);
+          st_hint(gscr + ((size_t)alpha * NB + beta) * prm.G + lc, z, pol_keep);
         }
     } else {
       constexpr int W = PB::W;
@@ -176,6 +216,17 @@ fourstep_kernel(const FourStepParams prm) {
         for (int m = 0; m < SB::R0; ++m)
           v[u * SB::R0 + m] = ldcg_cx(gscr + ((size_t)alpha * NB + SB::in_elem(tt, u, m)) * prm.G + lc);
       STB::run(smem_raw, v, tt, b, reinterpret_cast<const cx<T>*>(prm.twB));
+      // the task's scratch lines (NB rows x W columns) are consumed: drop them
+      // from L2 without a write-back
+      __syncthreads();
+      {
+        constexpr int LPR = W * (int)sizeof(cx<T>) / 128;  // lines per scratch row segment
+        for (int li = t; li < NB * LPR; li += kFsThreads) {
+          const int beta = li / LPR, part = li % LPR;
+          discard_l2(reinterpret_cast<const char*>(gscr + ((size_t)alpha * NB + beta) * prm.G + blk * W) +
+                     part * 128);
+        }
+      }
       if (valid) {
         cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging);
         const unsigned bmask = (1u << prm.band_shift) - 1u;
@@ -188,11 +239,12 @@ fourstep_kernel(const FourStepParams prm) {
             if constexpr (REDIR) {
               const int band = (int)(r >> prm.band_shift);
               if (band != prm.self_band) {
-                stg[(long long)band * prm.stg_band + (long long)(r & bmask) * prm.stg_within + c] = z;
+                st_hint(stg + (long long)band * prm.stg_band + (long long)(r & bmask) * prm.stg_within + c, z,
+                        pol_stream);
                 continue;
               }
             }
-            data[c + offset(r)] = z;
+            st_hint(data + c + offset(r), z, pol_stream);
           }
       }
     }
