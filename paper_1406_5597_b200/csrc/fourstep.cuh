@@ -39,7 +39,10 @@ struct FsPass {
   static constexpr int PS = SH::EB > 0 ? SH::EB : 30;
   // exchange column stride: S == 1 mod 16 words -> 16 adjacent columns per wavefront, no conflicts
   static constexpr int S = ((N + (N >> (PS > 20 ? 30 : PS)) + 15) / 16) * 16 + 1;
-  static constexpr bool SPLIT = sizeof(T) == 8;
+#ifndef TFFFT_FS_SPLIT
+#define TFFFT_FS_SPLIT 1
+#endif
+  static constexpr bool SPLIT = sizeof(T) == 8 && TFFFT_FS_SPLIT;
   static constexpr size_t SMEM = (SPLIT ? 8 : sizeof(cx<T>)) * (size_t)W * S;
 };
 
@@ -110,8 +113,11 @@ __device__ __forceinline__ void discard_l2(const void* a) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
 }
 
+#ifndef TFFFT_FS_MINB
+#define TFFFT_FS_MINB 3
+#endif
 template <typename T, int LA, int LB, bool INV, bool TWO, bool REDIR>
-__global__ void __launch_bounds__(kFsThreads)
+__global__ void __launch_bounds__(kFsThreads, TFFFT_FS_MINB)
 fourstep_kernel(const FourStepParams prm) {
   using PA = FsPass<T, LA>;
   using PB = FsPass<T, LB>;

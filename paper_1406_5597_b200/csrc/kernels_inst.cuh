@@ -4,6 +4,7 @@
 
 #include "kernels.cuh"
 #include "fourstep.cuh"
+#include "stage1_fused.cuh"
 
 namespace tffft {
 
@@ -156,6 +157,41 @@ static cudaError_t fs_dispatch(bool inv, int variant, const FourStepParams& p, c
     if (variant == 3) return fs_one<T, LA, LB, true, true, true>(p, s);
   }
   return cudaErrorInvalidValue;
+}
+
+template <typename T, int LR, int LC, bool FWD, bool REDIR>
+static cudaError_t s1_one(const Stage1Params& p, cudaStream_t s) {
+  const size_t sm = S1Cfg<T, LR, LC>::SMEM;
+  auto k = stage1_fused_kernel<T, LR, LC, FWD, REDIR>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  static int per_sm = [&] {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kS1Threads, sm);
+    return n < 1 ? 1 : n;
+  }();
+  (void)cudaGetLastError();
+  k<<<(unsigned)(per_sm * num_sms()), kS1Threads, sm, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int LR>
+static cudaError_t s1_dispatch(bool fwd, bool redir, const Stage1Params& p, cudaStream_t s) {
+  if (!fwd) return s1_one<T, LR, LR + 1, false, false>(p, s);
+  return redir ? s1_one<T, LR, LR + 1, true, true>(p, s) : s1_one<T, LR, LR + 1, true, false>(p, s);
+}
+
+template <>
+cudaError_t launch_stage1_fused<TFFFT_REAL>(int LR, int LC, bool fwd, bool redir, const Stage1Params& p,
+                                            cudaStream_t s) {
+  if (LC != LR + 1) return cudaErrorInvalidValue;
+  switch (LR) {
+    case 8: return s1_dispatch<TFFFT_REAL, 8>(fwd, redir, p, s);
+    case 9: return s1_dispatch<TFFFT_REAL, 9>(fwd, redir, p, s);
+    case 10: return s1_dispatch<TFFFT_REAL, 10>(fwd, redir, p, s);
+    case 11: return s1_dispatch<TFFFT_REAL, 11>(fwd, redir, p, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <>

@@ -27,6 +27,7 @@
 
 #include "../../include/tffft.h"
 #include "fourstep.cuh"
+#include "stage1_fused.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 
@@ -209,6 +210,9 @@ struct tffft_plan_s {
   void* fs_twA = nullptr;
   void* fs_twB = nullptr;
   void* fs_twN = nullptr;
+  // fused stage 1 (stage1_fused.cuh)
+  bool s1_fused = false;
+  unsigned* s1_counters = nullptr;
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -414,6 +418,34 @@ static RowParams row_params(tffft_plan_t pl, void* real, void* spec) {
   r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
   r.stats = pl->stats;
   return r;
+}
+
+// fused stage 1 / 1': one persistent kernel per direction, planes stay in L2
+static int stage1_fused(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaStream_t s) {
+  Stage1Params f{};
+  f.real = real;
+  f.spec = spec;
+  f.staging = (fwd && pl->p > 1) ? pl->staging : nullptr;
+  f.tw_row = pl->tw2;
+  f.tw_post = pl->tw2post;
+  f.tw_col = pl->tw1;
+  f.stats = pl->stats;
+  f.counters = pl->s1_counters;
+  f.n0p = pl->n0p;
+  f.n1 = pl->n1;
+  f.n2c = pl->n2c;
+  f.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
+  f.band_shift = ilog2(pl->n1p);
+  f.self_band = pl->rank;
+  f.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
+  f.stg_grp = (long long)pl->n1p * pl->n2c;
+  CUDA_TRY(cudaMemsetAsync(pl->s1_counters, 0, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p), s));
+  pl->launches++;
+  const cudaError_t e = pl->dtype == TFFFT_F64
+      ? launch_stage1_fused<double>(pl->L2h, pl->L1, fwd, f.staging != nullptr, f, s)
+      : launch_stage1_fused<float>(pl->L2h, pl->L1, fwd, f.staging != nullptr, f, s);
+  CUDA_TRY(e);
+  return TFFFT_OK;
 }
 
 static uint64_t wire_bytes(tffft_plan_t pl) {
@@ -647,8 +679,12 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
   }
   // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
   {
-    static const char* env_off = getenv("TFFFT_NO_FOURSTEP");
-    const int la = env_off ? 0 : fourstep_la(pl->L0);
+    // measured at 1024^3 (profiles/): the four-step wins for float32; for
+    // float64 the FP64 issue rate makes the direct 8-column kernel faster.
+    // TFFFT_FOURSTEP=0/1 overrides.
+    static const char* env_fs = getenv("TFFFT_FOURSTEP");
+    const bool want = env_fs ? atoi(env_fs) != 0 : dtype == TFFFT_F32;
+    const int la = want ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
       const long long ncols = (long long)pl->n1p * pl->n2c;
@@ -665,6 +701,14 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
       TRY(upload_table(pass_table(la), dtype, &pl->fs_twA, &ws));
       TRY(upload_table(pass_table(pl->L0 - la), dtype, &pl->fs_twB, &ws));
       TRY(upload_table(full_table(n0), dtype, &pl->fs_twN, &ws));
+    }
+  }
+  {
+    static const char* env_off = getenv("TFFFT_NO_FUSE");
+    if (!env_off && stage1_fused_supported(pl->L2h, pl->L1)) {
+      pl->s1_fused = true;
+      CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
+      ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
     }
   }
   pl->workspace = ws;
@@ -699,6 +743,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->pull_ptrs);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
+  cudaFree(pl->s1_counters);
   delete pl;
   return TFFFT_OK;
 }
@@ -734,9 +779,13 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
   StageEvents* ev;
   TRY(begin_events(pl, true, s, &ev));
   // stage 1: planes (dfft.py:161-163)
-  CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
   TRY(fabric_guard_staging(pl, s));
-  TRY(stage1_columns(pl, spec_out, false, s));
+  if (pl->s1_fused) {
+    TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
+  } else {
+    CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
+    TRY(stage1_columns(pl, spec_out, false, s));
+  }
   MARK(ev, 1, s);
   // exchange (exchange.py:263-276)
   if (pl->p > 1 && !pl->comm->is_nccl) TRY(fabric_pull_list(pl, spec_out, s));
@@ -766,8 +815,12 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   TRY(exchange(pl, spec, s));
   MARK(ev, 2, s);
   // stage 1' (dfft.py:206-209)
-  TRY(stage1_columns(pl, spec, true, s));
-  CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+  if (pl->s1_fused) {
+    TRY(stage1_fused(pl, real_out, spec, false, s));
+  } else {
+    TRY(stage1_columns(pl, spec, true, s));
+    CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+  }
   MARK(ev, 3, s);
   pl->last_inverse_stream = s;
   pl->inverse_ran = true;
