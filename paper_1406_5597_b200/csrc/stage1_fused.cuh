@@ -37,7 +37,31 @@ struct Stage1Params {
   double scale;
   int band_shift, self_band;          // forward redirect: band = n1 index >> band_shift
   long long stg_band, stg_grp;        // staging + band*stg_band + i*stg_grp + (e & mask)*n2c + k
+  int lookahead;                      // planes of A tasks handed out ahead of the B tasks
 };
+
+// Ticket order with lookahead D: A(0..D-1), then [A(q+D), B(q)] while q+D < ng,
+// then B(q) alone.  Returns isA, group, index within the group's task list.
+__device__ __forceinline__ void queue_decode(unsigned tk, int ng, int nA, int nB, int D, int& isA, int& g,
+                                             int& w) {
+  D = D < ng ? D : ng;
+  const unsigned head = (unsigned)D * (unsigned)nA;
+  if (tk < head) {
+    isA = 1; g = (int)(tk / (unsigned)nA); w = (int)(tk % (unsigned)nA);
+    return;
+  }
+  unsigned r = tk - head;
+  const unsigned full = (unsigned)(ng - D) * (unsigned)(nA + nB);
+  if (r < full) {
+    const int q = (int)(r / (unsigned)(nA + nB));
+    const int x = (int)(r % (unsigned)(nA + nB));
+    if (x < nA) { isA = 1; g = q + D; w = x; }
+    else { isA = 0; g = q; w = x - nA; }
+    return;
+  }
+  r -= full;
+  isA = 0; g = (ng - D) + (int)(r / (unsigned)nB); w = (int)(r % (unsigned)nB);
+}
 
 template <typename T, int LR, int LC>
 struct S1Cfg {
@@ -91,15 +115,7 @@ stage1_fused_kernel(const Stage1Params prm) {
         s_end = 1;
       } else {
         int isA, g, w;
-        if (tk < (unsigned)nA) {
-          isA = 1; g = 0; w = (int)tk;
-        } else {
-          const unsigned r = tk - (unsigned)nA;
-          const int q = (int)(r / (unsigned)(nA + nB));
-          const int x = (int)(r % (unsigned)(nA + nB));
-          if (q < ng - 1 && x < nA) { isA = 1; g = q + 1; w = x; }
-          else { isA = 0; g = q; w = q < ng - 1 ? x - nA : x; }
-        }
+        queue_decode(tk, ng, nA, nB, prm.lookahead, isA, g, w);
         if (!isA)
           while (ld_acquire(doneA + g) < (unsigned)nA) __nanosleep(64);
         s_end = 0; s_isA = isA; s_g = g; s_w = w;
@@ -182,6 +198,15 @@ stage1_fused_kernel(const Stage1Params prm) {
           }
         }
         __syncthreads();
+        // the spectral rows of this task are consumed (inverse clobbers its input,
+        // dfft.py:182-184): drop their whole L2 lines without a write-back
+        if (t < CF::BR * (int)(sizeof(cx<T>) * 2 * NR / 128 + 2)) {
+          const char* lo = reinterpret_cast<const char*>(spec + ((long long)plane * n1 + (long long)w * CF::BR) * n2c);
+          const char* hi = lo + (size_t)CF::BR * n2c * sizeof(cx<T>);
+          const char* first = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(lo) + 127) & ~(uintptr_t)127);
+          const char* line = first + (size_t)t * 128;
+          if (line + 128 <= hi) discard_l2(line);
+        }
         const cx<T>* twpp = twp;
         cx<T> v[SR::E];
 #pragma unroll

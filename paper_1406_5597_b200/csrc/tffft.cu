@@ -439,6 +439,10 @@ static int stage1_fused(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaS
   f.self_band = pl->rank;
   f.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
   f.stg_grp = (long long)pl->n1p * pl->n2c;
+  {
+    static const char* env = getenv("TFFFT_S1_LOOKAHEAD");
+    f.lookahead = env ? std::max(1, atoi(env)) : 3;
+  }
   CUDA_TRY(cudaMemsetAsync(pl->s1_counters, 0, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p), s));
   pl->launches++;
   const cudaError_t e = pl->dtype == TFFFT_F64
