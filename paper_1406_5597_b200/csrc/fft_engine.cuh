@@ -223,8 +223,13 @@ struct Shape {
 // Exchange buffer: element a of transform b at b*S + a + (a >> PS).  With
 // SPLIT (float64) the exchange runs in two rounds of 8-byte words (real parts,
 // then imaginary parts), halving the buffer; otherwise whole complex values.
-template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false>
+// WARP: every transform's TPT threads sit in one warp, so the exchanges only
+// need __syncwarp (no CTA-wide barrier).
+template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, bool WARP = false>
 struct Stockham {
+  static __device__ __forceinline__ void sync() {
+    if constexpr (WARP) __syncwarp(); else __syncthreads();
+  }
   using SH = Shape<L>;
   static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;
 
@@ -289,18 +294,18 @@ struct Stockham {
   static __device__ __forceinline__ void exchange(void* sm, cx<T>* v, int tt, int b) {
     if constexpr (SPLIT) {
       store<p - 1, 0>(sm, v, tt, b);
-      __syncthreads();
+      sync();
       load<p, 0>(sm, v, tt, b);
-      __syncthreads();
+      sync();
       store<p - 1, 1>(sm, v, tt, b);
-      __syncthreads();
+      sync();
       load<p, 1>(sm, v, tt, b);
-      __syncthreads();
+      sync();
     } else {
       store<p - 1, 2>(sm, v, tt, b);
-      __syncthreads();
+      sync();
       load<p, 2>(sm, v, tt, b);
-      __syncthreads();
+      sync();
     }
   }
 

@@ -683,11 +683,12 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
   }
   // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
   {
-    // measured at 1024^3 (profiles/): the four-step wins for float32; for
-    // float64 the FP64 issue rate makes the direct 8-column kernel faster.
-    // TFFFT_FOURSTEP=0/1 overrides.
+    // measured at 1024^3 (profiles/r01_*): the four-step moves exactly the
+    // algorithmic bytes with 1 KB row visits but issues ~60% more instructions per
+    // element than the direct 8-column kernel, which is faster today; opt-in
+    // with TFFFT_FOURSTEP=1.
     static const char* env_fs = getenv("TFFFT_FOURSTEP");
-    const bool want = env_fs ? atoi(env_fs) != 0 : dtype == TFFFT_F32;
+    const bool want = env_fs ? atoi(env_fs) != 0 : false;
     const int la = want ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
@@ -708,8 +709,11 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
     }
   }
   {
-    static const char* env_off = getenv("TFFFT_NO_FUSE");
-    if (!env_off && stage1_fused_supported(pl->L2h, pl->L1)) {
+    // measured at 1024^3 (profiles/r01_*): the fused persistent stage 1 keeps the
+    // planes in L2 but its mixed row/column tasks run at lower occupancy; the two
+    // streaming kernels are faster today, so fusion is opt-in (TFFFT_FUSE=1)
+    static const char* env_fuse = getenv("TFFFT_FUSE");
+    if (env_fuse && atoi(env_fuse) != 0 && stage1_fused_supported(pl->L2h, pl->L1)) {
       pl->s1_fused = true;
       CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
