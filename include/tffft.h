@@ -75,6 +75,16 @@ int tffft_comm_destroy(tffft_comm_t comm);
  * (layout.py:83-93).  pattern: TFFFT_PAIRWISE (chunk-granular in-place landing). */
 int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm_t comm,
                       tffft_plan_t* plan);
+/* algorithm flags for tffft_plan_create_ex (0 = the default kernels) */
+enum {
+  TFFFT_FLAG_FUSED_STAGE1 = 1,   /* one persistent kernel per direction for stage 1 (planes in L2) */
+  TFFFT_FLAG_FOURSTEP_STAGE3 = 2 /* stage 3 as an L2-resident four-step with 1 KB row visits */
+};
+/* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
+int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
+                         tffft_plan_t* plan);
+/* algorithm flags actually in effect (a flag is dropped when the grid has no such kernel) */
+int tffft_plan_flags(tffft_plan_t plan, int* flags);
 /* device bytes owned by the plan (staging, twiddles, statistics) */
 int tffft_plan_workspace_bytes(tffft_plan_t plan, size_t* bytes);
 /* element counts: real slab n0/p*n1*n2 reals, spectral slab n1/p*n0*(n2/2+1) complex */

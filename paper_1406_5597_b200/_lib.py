@@ -29,6 +29,9 @@ _SIGS = {
     "tffft_comm_destroy": (_c.c_int, [_c.c_void_p]),
     "tffft_plan_create": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_void_p,
                                      _c.POINTER(_c.c_void_p)]),
+    "tffft_plan_create_ex": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
+                                        _c.c_void_p, _c.POINTER(_c.c_void_p)]),
+    "tffft_plan_flags": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_plan_workspace_bytes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_size_t)]),
     "tffft_plan_sizes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_int64)]),
     "tffft_plan_destroy": (_c.c_int, [_c.c_void_p]),

@@ -631,7 +631,28 @@ int tffft_comm_destroy(tffft_comm_t c) {
   return TFFFT_OK;
 }
 
+static int env_flags() {
+  int f = 0;
+  const char* fuse = getenv("TFFFT_FUSE");
+  const char* fs = getenv("TFFFT_FOURSTEP");
+  if (fuse && atoi(fuse) != 0) f |= TFFFT_FLAG_FUSED_STAGE1;
+  if (fs && atoi(fs) != 0) f |= TFFFT_FLAG_FOURSTEP_STAGE3;
+  return f;
+}
+
 int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm_t comm, tffft_plan_t* out) {
+  return tffft_plan_create_ex(n0, n1, n2, dtype, pattern, -1, comm, out);
+}
+
+int tffft_plan_flags(tffft_plan_t pl, int* flags) {
+  if (!pl || !flags) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0);
+  return TFFFT_OK;
+}
+
+int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
+                         tffft_plan_t* out) {
+  if (flags < 0) flags = env_flags();
   if (!comm || !out) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   const int p = comm->p;
   // layout.py:63-66 (powers of two), layout.py:83-93 (validate)
@@ -687,9 +708,7 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
     // algorithmic bytes with 1 KB row visits but issues ~60% more instructions per
     // element than the direct 8-column kernel, which is faster today; opt-in
     // with TFFFT_FOURSTEP=1.
-    static const char* env_fs = getenv("TFFFT_FOURSTEP");
-    const bool want = env_fs ? atoi(env_fs) != 0 : false;
-    const int la = want ? fourstep_la(pl->L0) : 0;
+    const int la = (flags & TFFFT_FLAG_FOURSTEP_STAGE3) ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
       const long long ncols = (long long)pl->n1p * pl->n2c;
@@ -712,8 +731,7 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
     // measured at 1024^3 (profiles/r01_*): the fused persistent stage 1 keeps the
     // planes in L2 but its mixed row/column tasks run at lower occupancy; the two
     // streaming kernels are faster today, so fusion is opt-in (TFFFT_FUSE=1)
-    static const char* env_fuse = getenv("TFFFT_FUSE");
-    if (env_fuse && atoi(env_fuse) != 0 && stage1_fused_supported(pl->L2h, pl->L1)) {
+    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && stage1_fused_supported(pl->L2h, pl->L1)) {
       pl->s1_fused = true;
       CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);

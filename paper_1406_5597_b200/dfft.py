@@ -92,6 +92,12 @@ class FftPlan:
         return int(n.value)
 
     @property
+    def algorithms(self) -> tuple[str, ...]:
+        f = ctypes.c_int()
+        _lib.check(_lib.lib().tffft_plan_flags(self.handle, ctypes.byref(f)))
+        return tuple(a for a, bit in ALGORITHM_FLAGS.items() if f.value & bit)
+
+    @property
     def workspace_bytes(self) -> int:
         n = ctypes.c_size_t()
         _lib.check(_lib.lib().tffft_plan_workspace_bytes(self.handle, ctypes.byref(n)))
@@ -109,10 +115,17 @@ class FftPlan:
             pass
 
 
+ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2}
+
+
 def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED,
          comm_pattern: CommPattern = CommPattern.PAIRWISE, dtype: str = "float64",
-         check_consistency: bool = True) -> FftPlan:
-    """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric."""
+         check_consistency: bool = True, algorithms: tuple[str, ...] | None = None) -> FftPlan:
+    """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric.
+
+    ``algorithms`` selects optional kernel schedules ("fused_stage1",
+    "fourstep_stage3"); None takes the library defaults (TFFFT_FUSE /
+    TFFFT_FOURSTEP environment switches)."""
     validate(grid, comm.p)
     if strategy is not Strategy.STRIDED:
         raise ConfigurationError("the B200 path implements the transpose-free STRIDED strategy only")
@@ -121,10 +134,16 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     if dtype not in DTYPES:
         raise ConfigurationError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
     code, rdt, cdt = DTYPES[dtype]
+    flags = -1
+    if algorithms is not None:
+        unknown = set(algorithms) - set(ALGORITHM_FLAGS)
+        if unknown:
+            raise ConfigurationError(f"unknown algorithms {sorted(unknown)}; choose from {sorted(ALGORITHM_FLAGS)}")
+        flags = sum(ALGORITHM_FLAGS[a] for a in set(algorithms))
     h = ctypes.c_void_p()
     with torch.cuda.device(comm.device):
-        _lib.check(_lib.lib().tffft_plan_create(grid.n0, grid.n1, grid.n2, code, 0, comm.handle,
-                                                ctypes.byref(h)))
+        _lib.check(_lib.lib().tffft_plan_create_ex(grid.n0, grid.n1, grid.n2, code, 0, flags, comm.handle,
+                                                   ctypes.byref(h)))
         p, rank = comm.p, comm.rank
         dev = torch.device("cuda", comm.device)
         work1 = torch.empty((grid.n0 // p) * grid.n1 * grid.n2c, dtype=cdt, device=dev)
