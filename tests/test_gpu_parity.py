@@ -151,3 +151,63 @@ def test_counters_and_timers():
         assert set(timers) == {"stage1_us", "exchange_us", "stage3_us"}
         assert all(v >= 0 for v in timers.values())
         assert launches >= 6
+
+
+ALG_CASES = [
+    # fused stage 1 needs n1 == n2 in [512, 4096]; the four-step needs n0 in [512, 4096]
+    ((4, 512, 512), 1, ("fused_stage1",)),
+    ((8, 512, 512), 2, ("fused_stage1",)),
+    ((512, 4, 8), 1, ("fourstep_stage3",)),
+    ((512, 8, 16), 2, ("fourstep_stage3",)),
+    ((1024, 4, 4), 4, ("fourstep_stage3",)),
+    ((2048, 2, 4), 2, ("fourstep_stage3",)),
+    ((4096, 2, 2), 1, ("fourstep_stage3",)),
+    ((8, 1024, 1024), 2, ("fused_stage1", "fourstep_stage3")),
+]
+
+
+@pytest.mark.parametrize("shape,p,algs", ALG_CASES, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_optional_schedules_vs_oracle(shape, p, algs, dtype):
+    """The opt-in kernel schedules (fused persistent stage 1, L2-resident
+    four-step stage 3) against the oracle, forward and round trip."""
+    x = oracle.uniform_field(shape, seed=7 + p)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dtype, algorithms=algs)
+        assert set(fp.algorithms) == set(algs)
+        spec = tf.forward(fp, slabs[ep.rank])
+        f = spec.data.cpu().numpy().copy()
+        back = tf.inverse(fp, spec)
+        return f, back.data.cpu().numpy().copy()
+
+    res = tf.run_spmd(p, body)
+    ref = oracle.forward_all(x, p)
+    for q in range(p):
+        assert rel(res[q][0], ref[q]) <= TOL[dtype]
+    back = np.concatenate([r[1].reshape(-1) for r in res]).reshape(shape)
+    assert rel(back, x) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("algs", [(), ("fused_stage1", "fourstep_stage3")], ids=["default", "fused+fourstep"])
+def test_512_cubed_normal_vs_torch_fft(algs):
+    """BASELINE config 3 (512^3 float64 standard normal, p=1) at full size:
+    forward against torch.fft.rfftn (test-only reference) and round trip."""
+    import torch
+    n = 512
+    grid = tf.GlobalGrid(n, n, n)
+    ep = tf.make_communicators(1)[0]
+    fp = tf.plan(grid, ep, algorithms=algs)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(n * n * n, dtype=torch.float64, device="cuda", generator=g)
+    spec = tf.forward(fp, tf.RealSlab(fp.real_layout, x))
+    ref = torch.fft.rfftn(x.view(n, n, n))
+    err = (torch.linalg.norm(spec.data.view(n, n, n // 2 + 1) - ref) / torch.linalg.norm(ref)).item()
+    assert err <= 1e-12
+    back = tf.inverse(fp, spec)
+    rt = (torch.linalg.norm(back.data - x) / torch.linalg.norm(x)).item()
+    assert rt <= 1e-12
