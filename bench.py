@@ -330,7 +330,7 @@ def main():
     ap.add_argument("--grid", type=int, default=1024)
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-planes", type=int, default=32)
+    ap.add_argument("--cpu-planes", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
