@@ -223,12 +223,14 @@ struct Shape {
 // Exchange buffer: element a of transform b at b*S + a + (a >> PS).  With
 // SPLIT (float64) the exchange runs in two rounds of 8-byte words (real parts,
 // then imaginary parts), halving the buffer; otherwise whole complex values.
-// WARP: every transform's TPT threads sit in one warp, so the exchanges only
-// need __syncwarp (no CTA-wide barrier).
-template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, bool WARP = false>
+// SYNC: 0 = __syncthreads; 32 = __syncwarp (every transform inside one warp);
+// otherwise named barrier 1 over the first SYNC threads (warp-specialised CTAs).
+template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0>
 struct Stockham {
   static __device__ __forceinline__ void sync() {
-    if constexpr (WARP) __syncwarp(); else __syncthreads();
+    if constexpr (SYNC == 0) __syncthreads();
+    else if constexpr (SYNC == 32) __syncwarp();
+    else asm volatile("bar.sync 1, %0;" ::"n"(SYNC) : "memory");
   }
   using SH = Shape<L>;
   static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;

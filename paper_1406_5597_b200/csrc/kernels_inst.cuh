@@ -5,6 +5,7 @@
 #include "kernels.cuh"
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
+#include "fourstep_tma.cuh"
 
 namespace tffft {
 
@@ -190,6 +191,32 @@ cudaError_t launch_stage1_fused<TFFFT_REAL>(int LR, int LC, bool fwd, bool redir
     case 9: return s1_dispatch<TFFFT_REAL, 9>(fwd, redir, p, s);
     case 10: return s1_dispatch<TFFFT_REAL, 10>(fwd, redir, p, s);
     case 11: return s1_dispatch<TFFFT_REAL, 11>(fwd, redir, p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int LA, int LB, bool INV>
+static cudaError_t ft_one(const CUtensorMap* maps, const FsTmaParams& p, cudaStream_t s) {
+  const size_t sm = FtCfg<T, LA, LB>::SMEM;
+  auto k = fourstep_tma_kernel<T, LA, LB, INV>;
+  static cudaError_t prep = prep_smem(k, sm);
+  if (prep != cudaSuccess) return prep;
+  static int per_sm = [&] {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFtThreads, sm);
+    return n < 1 ? 1 : n;
+  }();
+  (void)cudaGetLastError();
+  k<<<(unsigned)(per_sm * num_sms()), kFtThreads, sm, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* maps, const FsTmaParams& p,
+                                            cudaStream_t s) {
+  switch (L) {
+    case 10: return inv ? ft_one<TFFFT_REAL, 5, 5, true>(maps, p, s) : ft_one<TFFFT_REAL, 5, 5, false>(maps, p, s);
+    case 12: return inv ? ft_one<TFFFT_REAL, 6, 6, true>(maps, p, s) : ft_one<TFFFT_REAL, 6, 6, false>(maps, p, s);
     default: return cudaErrorInvalidValue;
   }
 }

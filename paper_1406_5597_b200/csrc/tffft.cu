@@ -28,6 +28,7 @@
 #include "../../include/tffft.h"
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
+#include "fourstep_tma.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 
@@ -341,6 +342,79 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   return TFFFT_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// rank-r map over `base` in real elements of the plan's precision; dims/strides innermost first
+static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const cuuint64_t* dims,
+                    const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(m, pl->dtype == TFFFT_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        (cuuint32_t)rank, base, dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TFFFT_OK;
+}
+
+// stage 3 at p = 1 through the TMA-fed four-step (fourstep_tma.cuh)
+static int stage3_tma(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  const int la = pl->fs_la, lb = pl->L0 - la;
+  const long long NA = 1LL << la, NB = 1LL << lb, N = (long long)pl->n0;
+  const long long W = 256 / (NA / 8);  // columns per task: 256 threads, NA / 8 threads per column
+  const long long ncols = (long long)pl->n1 * pl->n2c;
+  const long long esz = (long long)pl->esz, S1 = ncols * esz, G = pl->fs_G;
+  CUtensorMap maps[4];
+  {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * ncols), (cuuint64_t)NA, (cuuint64_t)NB};
+    cuuint64_t st[2] = {(cuuint64_t)(NB * S1), (cuuint64_t)S1};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)NA, 1};
+    TRY(make_map(pl, &maps[0], spec, 3, d, st, box));
+  }
+  {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * ncols), (cuuint64_t)NB, (cuuint64_t)NA};
+    cuuint64_t st[2] = {(cuuint64_t)(NA * S1), (cuuint64_t)S1};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)NB, 1};
+    TRY(make_map(pl, &maps[1], spec, 3, d, st, box));
+  }
+  {
+    cuuint64_t d[4] = {(cuuint64_t)(2 * G), (cuuint64_t)NA, (cuuint64_t)NB, (cuuint64_t)kFsSlots};
+    cuuint64_t st[3] = {(cuuint64_t)(NB * G * esz), (cuuint64_t)(G * esz), (cuuint64_t)(N * G * esz)};
+    cuuint32_t boxa[4] = {(cuuint32_t)(2 * W), (cuuint32_t)NA, 1, 1};
+    cuuint32_t boxb[4] = {(cuuint32_t)(2 * W), 1, (cuuint32_t)NB, 1};
+    TRY(make_map(pl, &maps[2], pl->fs_scratch, 4, d, st, boxa));
+    TRY(make_map(pl, &maps[3], pl->fs_scratch, 4, d, st, boxb));
+  }
+  FsTmaParams f{};
+  f.twA = pl->fs_twA;
+  f.twB = pl->fs_twB;
+  f.twN = pl->fs_twN;
+  f.counters = pl->fs_counters;
+  f.ngroups = pl->fs_groups;
+  f.G = pl->fs_G;
+  CUDA_TRY(cudaMemsetAsync(pl->fs_counters, 0, sizeof(unsigned) * (1 + 2 * (size_t)pl->fs_groups), s));
+  pl->launches++;
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_fourstep_tma<double>(pl->L0, inv, maps, f, s)
+                                               : launch_fourstep_tma<float>(pl->L0, inv, maps, f, s);
+  CUDA_TRY(e);
+  return TFFFT_OK;
+}
+
 static cudaError_t fs_launch(tffft_plan_t pl, bool inv, int variant, const FourStepParams& prm, cudaStream_t s) {
   pl->launches++;
   return pl->dtype == TFFFT_F64 ? launch_fourstep<double>(pl->L0, inv, variant, prm, s)
@@ -349,6 +423,8 @@ static cudaError_t fs_launch(tffft_plan_t pl, bool inv, int variant, const FourS
 
 // stage 3 / 3': c2c along n0 of every STRIDED_INPLACE column c = j*n2c + k
 static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  if (pl->fs_la > 0 && pl->p == 1 && fourstep_tma_supported(pl->L0) && !getenv("TFFFT_NO_TMA"))
+    return stage3_tma(pl, spec, inv, s);
   if (pl->fs_la > 0) {
     FourStepParams f{};
     f.data = spec;

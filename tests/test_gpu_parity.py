@@ -162,6 +162,8 @@ ALG_CASES = [
     ((1024, 4, 4), 4, ("fourstep_stage3",)),
     ((2048, 2, 4), 2, ("fourstep_stage3",)),
     ((4096, 2, 2), 1, ("fourstep_stage3",)),
+    ((1024, 8, 8), 1, ("fourstep_stage3",)),      # TMA-fed four-step (p = 1)
+    ((1024, 16, 64), 1, ("fourstep_stage3",)),
     ((8, 1024, 1024), 2, ("fused_stage1",)),
 ]
 
