@@ -34,6 +34,7 @@ struct FsTmaParams {
   const void* twB;
   const void* twN;
   unsigned* counters;  // [0] ticket, [1, 1+ng) doneA, [1+ng, 1+2ng) doneB
+  const void* scratch; // for discarding consumed scratch lines
   int ngroups, G;
 };
 
@@ -62,32 +63,48 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         : "memory");
   }
 }
-__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+// TMA tile moves with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                          uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                          uint64_t* bar) {
+                                          uint64_t* bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
-               ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int c0, int c1, int c2, const void* src,
+                                           uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src)), "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void tma_store4(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
-               ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+__device__ __forceinline__ void tma_store4(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src,
+                                           uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src)), "l"(pol)
                : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
+  unsigned done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kFtConsumers) : "memory"); }
@@ -148,10 +165,14 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
   if (warp == kFtConsumers / 32) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_norm = policy_evict_last();
+      unsigned next_tk = atomicAdd(prm.counters, 1u);  // one ticket ahead: the atomic's latency is hidden
       for (unsigned i = 0;; ++i) {
         const int s = i % kFtStages;
+        const unsigned tk = next_tk;
+        if (tk < total) next_tk = atomicAdd(prm.counters, 1u);
         mbar_wait(empty + s, ((i / kFtStages) & 1) ^ 1);
-        const unsigned tk = atomicAdd(prm.counters, 1u);
         int* d = desc + 4 * s;
         if (tk >= total) {
           d[0] = 1;
@@ -172,10 +193,10 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
         cx<T>* dst = stage0 + (size_t)s * (CF::STAGE / sizeof(cx<T>));
         if (isA) {
           const int beta = w / blocks, blk = w % blocks;
-          tma_load3(dst, &map_in, 2 * (g * prm.G + blk * W), 0, beta, full + s);
+          tma_load3(dst, &map_in, 2 * (g * prm.G + blk * W), 0, beta, full + s, pol_stream);
         } else {
           const int alpha = w / blocks, blk = w % blocks;
-          tma_load4(dst, &map_scr_b, 2 * blk * W, alpha, 0, g % kFsSlots, full + s);
+          tma_load4(dst, &map_scr_b, 2 * blk * W, alpha, 0, g % kFsSlots, full + s, pol_norm);
         }
       }
     }
@@ -183,28 +204,51 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
   }
   if (warp == kFtConsumers / 32 + 1) {
     // ------------------------------------------------------------ store
+    // Up to two stores in flight; a task is published (done counter) once its
+    // writes are complete.  When no further task is ready the warp flushes, so
+    // a producer waiting on a done counter never waits on an idle store warp.
     if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      int pend_isA = -1, pend_g = 0;  // stored, not yet published
+      auto publish = [&](int isA, int g) {
+        fence_async_global();
+        __threadfence();
+        atomicAdd(isA ? doneA + g : doneB + g, 1u);
+      };
       for (unsigned i = 0;; ++i) {
         const int s = i % kFtStages;
-        mbar_wait(ready + s, (i / kFtStages) & 1);
+        const unsigned par = (i / kFtStages) & 1;
+        if (pend_isA >= 0 && !mbar_test(ready + s, par)) {
+          bulk_wait0();
+          publish(pend_isA, pend_g);
+          pend_isA = -1;
+        }
+        mbar_wait(ready + s, par);
         const int* d = desc + 4 * s;
         if (d[0]) break;
         const int isA = d[1], g = d[2], w = d[3];
         const cx<T>* src = stage0 + (size_t)s * (CF::STAGE / sizeof(cx<T>));
         if (isA) {
           const int beta = w / blocks, blk = w % blocks;
-          tma_store4(&map_scr_a, 2 * blk * W, 0, beta, g % kFsSlots, src);
+          tma_store4(&map_scr_a, 2 * blk * W, 0, beta, g % kFsSlots, src, pol_keep);
         } else {
           const int alpha = w / blocks, blk = w % blocks;
-          tma_store3(&map_out, 2 * (g * prm.G + blk * W), 0, alpha, src);
+          tma_store3(&map_out, 2 * (g * prm.G + blk * W), 0, alpha, src, pol_stream);
         }
         bulk_commit();
         bulk_wait_read0();
         mbar_arrive(empty + s);  // the producer may refill the stage
-        bulk_wait0();            // writes complete: publish the task
-        fence_async_global();
-        __threadfence();
-        atomicAdd(isA ? doneA + g : doneB + g, 1u);
+        if (pend_isA >= 0) {
+          bulk_wait1();  // the previous store's writes are complete
+          publish(pend_isA, pend_g);
+        }
+        pend_isA = isA;
+        pend_g = g;
+      }
+      if (pend_isA >= 0) {
+        bulk_wait0();
+        publish(pend_isA, pend_g);
       }
     }
     return;
@@ -225,6 +269,12 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
     cx<T>* st = stage0 + (size_t)s * (CF::STAGE / sizeof(cx<T>));
     if (isA) {
       const int beta = w / blocks;
+      cx<T> tw8[SA::E];  // epilogue twiddles issued before the FFT so their latency hides behind it
+#pragma unroll
+      for (int u = 0; u < SA::E / SA::RL; ++u)
+#pragma unroll
+        for (int m = 0; m < SA::RL; ++m)
+          tw8[u * SA::RL + m] = ldg_cx(twN + ((beta * SA::out_elem(tt, u, m)) & (N - 1)));
       cx<T> v[SA::E];
 #pragma unroll
       for (int u = 0; u < SA::E / SA::R0; ++u)
@@ -237,9 +287,17 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
 #pragma unroll
         for (int m = 0; m < SA::RL; ++m) {
           const int alpha = SA::out_elem(tt, u, m);
-          st[alpha * W + b] = ctw<INV>(v[u * SA::RL + m], ldg_cx(twN + ((beta * alpha) & (N - 1))));
+          st[alpha * W + b] = ctw<INV>(v[u * SA::RL + m], tw8[u * SA::RL + m]);
         }
     } else {
+      {  // the task's scratch tile has landed in shared memory: drop it from L2 unwritten
+        const int g = d[2], alpha = w / blocks, blk = w % blocks;
+        constexpr int LPR = W * (int)sizeof(cx<T>) / 128;
+        const char* base = reinterpret_cast<const char*>(prm.scratch) +
+                           ((((size_t)(g % kFsSlots) * N + (size_t)alpha * NB) * prm.G) + (size_t)blk * W) * sizeof(cx<T>);
+        for (int li = t; li < NB * LPR; li += kFtConsumers)
+          discard_l2(base + (size_t)(li / LPR) * prm.G * sizeof(cx<T>) + (li % LPR) * 128);
+      }
       cx<T> v[SB::E];
 #pragma unroll
       for (int u = 0; u < SB::E / SB::R0; ++u)

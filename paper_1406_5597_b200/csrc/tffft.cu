@@ -405,6 +405,7 @@ static int stage3_tma(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
   f.twB = pl->fs_twB;
   f.twN = pl->fs_twN;
   f.counters = pl->fs_counters;
+  f.scratch = pl->fs_scratch;
   f.ngroups = pl->fs_groups;
   f.G = pl->fs_G;
   CUDA_TRY(cudaMemsetAsync(pl->fs_counters, 0, sizeof(unsigned) * (1 + 2 * (size_t)pl->fs_groups), s));
