@@ -65,9 +65,14 @@ struct FourStepParams {
   long long stg_band, stg_within;
 };
 
+// Poll a completion counter.  A relaxed (not acquire) load: ld.acquire.gpu
+// compiles to CCTL.IVALL, which would invalidate this SM's whole L1 (and the
+// twiddle tables in it) on every poll.  Every read of the data a counter
+// publishes bypasses L1 (ld.global.cg or TMA) and the producer publishes with
+// a fence + atomic after its writes completed, so L2 already holds the data.
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 

@@ -180,7 +180,7 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
           break;
         }
         int isA, g, w;
-        queue_decode(tk, ng, nA, nB, 1, isA, g, w);
+        queue_decode(tk, ng, nA, nB, 2, isA, g, w);  // A(g) runs two groups ahead of B(g); 3 ring slots
         if (isA) {
           if (g >= kFsSlots)
             while (ld_acquire(doneB + (g - kFsSlots)) < (unsigned)nB) __nanosleep(64);
