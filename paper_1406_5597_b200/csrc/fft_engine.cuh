@@ -85,6 +85,11 @@ __device__ __forceinline__ cx<T> ldg_cx(const cx<T>* p) {
   auto v = __ldg(reinterpret_cast<const typename vec2<T>::type*>(p));
   return {v.x, v.y};
 }
+// twiddle fetch from global (read-only path) or, with TWS, from a shared-memory copy
+template <bool TWS, typename T>
+__device__ __forceinline__ cx<T> tw_cx(const cx<T>* p) {
+  if constexpr (TWS) return *p; else return ldg_cx(p);
+}
 
 // w^m for m = 1..R-1 by a balanced product tree (depth <= log2 R), from one
 // table load instead of R-1: trades L1 wavefronts for idle FP64 issue slots.
@@ -225,7 +230,7 @@ struct Shape {
 // then imaginary parts), halving the buffer; otherwise whole complex values.
 // SYNC: 0 = __syncthreads; 32 = __syncwarp (every transform inside one warp);
 // otherwise named barrier 1 over the first SYNC threads (warp-specialised CTAs).
-template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0>
+template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0, bool TWS = false>
 struct Stockham {
   static __device__ __forceinline__ void sync() {
     if constexpr (SYNC == 0) __syncthreads();
@@ -247,7 +252,7 @@ struct Stockham {
         const int j = tt + TPT * u;
         const int k = j & (NS - 1);
         cx<T> pw[R];
-        twiddle_powers<R>(ldg_cx(tw + tw_offset(L, p) + k), pw);
+        twiddle_powers<R>(tw_cx<TWS>(tw + tw_offset(L, p) + k), pw);
 #pragma unroll
         for (int m = 1; m < R; ++m) v[u * R + m] = ctw<INV>(v[u * R + m], pw[m]);
       }

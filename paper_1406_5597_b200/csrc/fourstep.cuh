@@ -76,6 +76,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+// Publish a finished task: release-ordered add.  Unlike __threadfence() +
+// atomicAdd (a gpu-scope fence, CCTL.IVALL in SASS) it does not invalidate
+// the SM's L1.  Called by one thread after a CTA barrier, so the release
+// covers the whole CTA's writes (cumulativity).
+__device__ __forceinline__ void publish_add(unsigned* p) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ cx<T> ldcg_cx(const cx<T>* p) {
   auto v = __ldcg(reinterpret_cast<const typename vec2<T>::type*>(p));
@@ -260,10 +268,7 @@ fourstep_kernel(const FourStepParams prm) {
       }
     }
     __syncthreads();  // every thread's stores issued before the completion count
-    if (t == 0) {
-      __threadfence();
-      atomicAdd(isA ? doneA + g : doneB + g, 1u);
-    }
+    if (t == 0) publish_add(isA ? doneA + g : doneB + g);
   }
 }
 

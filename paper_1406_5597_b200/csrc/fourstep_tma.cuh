@@ -118,7 +118,10 @@ struct FtCfg {
   static constexpr int W = PA::W;
   static constexpr size_t STAGE = sizeof(cx<T>) * (size_t)W * (NA > NB ? NA : NB);
   static constexpr size_t XCHG = PA::SMEM > PB::SMEM ? PA::SMEM : PB::SMEM;
-  static constexpr size_t SMEM = kFtStages * STAGE + XCHG + 1024;  // + barriers / descriptors
+  // twiddles copied into shared memory per CTA: pass tables of both lengths + w_N^t, t < N
+  static constexpr int TWA = Shape<LA>::TW > 0 ? Shape<LA>::TW : 1, TWB = Shape<LB>::TW > 0 ? Shape<LB>::TW : 1;
+  static constexpr size_t TWBYTES = sizeof(cx<T>) * (size_t)(TWA + TWB + NA * NB);
+  static constexpr size_t SMEM = kFtStages * STAGE + XCHG + TWBYTES + 1024;  // + barriers / descriptors
 };
 
 template <typename T, int LA, int LB, bool INV>
@@ -132,13 +135,16 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
   using PA = FsPass<T, LA>;
   using PB = FsPass<T, LB>;
   constexpr int NA = CF::NA, NB = CF::NB, N = NA * NB, W = CF::W;
-  using STA = Stockham<T, LA, INV, PA::S, PA::PS, PA::SPLIT, kFtConsumers>;
-  using STB = Stockham<T, LB, INV, PB::S, PB::PS, PB::SPLIT, kFtConsumers>;
+  using STA = Stockham<T, LA, INV, PA::S, PA::PS, PA::SPLIT, kFtConsumers, true>;
+  using STB = Stockham<T, LB, INV, PB::S, PB::PS, PB::SPLIT, kFtConsumers, true>;
 
   extern __shared__ __align__(1024) unsigned char smem_tma[];
   cx<T>* stage0 = reinterpret_cast<cx<T>*>(smem_tma);
   unsigned char* xbuf = smem_tma + kFtStages * CF::STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + CF::XCHG);
+  cx<T>* s_twA = reinterpret_cast<cx<T>*>(xbuf + CF::XCHG);
+  cx<T>* s_twB = s_twA + CF::TWA;
+  cx<T>* s_twN = s_twB + CF::TWB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_twA) + CF::TWBYTES);
   uint64_t* empty = full + kFtStages;
   uint64_t* ready = empty + kFtStages;
   int* desc = reinterpret_cast<int*>(ready + kFtStages);  // [stage][4]: end, isA, g, w
@@ -160,6 +166,14 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  {  // twiddles -> shared memory (an L1 invalidation by a completion fence cannot evict them)
+    const cx<T>* ga = reinterpret_cast<const cx<T>*>(prm.twA);
+    const cx<T>* gb = reinterpret_cast<const cx<T>*>(prm.twB);
+    const cx<T>* gn = reinterpret_cast<const cx<T>*>(prm.twN);
+    for (int k = t; k < CF::TWA; k += kFtThreads) s_twA[k] = ga[k];
+    for (int k = t; k < CF::TWB; k += kFtThreads) s_twB[k] = gb[k];
+    for (int k = t; k < N; k += kFtThreads) s_twN[k] = gn[k];
+  }
   __syncthreads();
 
   if (warp == kFtConsumers / 32) {
@@ -180,14 +194,13 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
           break;
         }
         int isA, g, w;
-        queue_decode(tk, ng, nA, nB, 2, isA, g, w);  // A(g) runs two groups ahead of B(g); 3 ring slots
+        queue_decode(tk, ng, nA, nB, 1, isA, g, w);  // A(g+1) interleaves with B(g); A(g) needs B(g-3): 3 ring slots
         if (isA) {
           if (g >= kFsSlots)
             while (ld_acquire(doneB + (g - kFsSlots)) < (unsigned)nB) __nanosleep(64);
         } else {
           while (ld_acquire(doneA + g) < (unsigned)nA) __nanosleep(64);
         }
-        fence_async_global();
         d[0] = 0; d[1] = isA; d[2] = g; d[3] = w;
         mbar_arrive_tx(full + s, (unsigned)((isA ? NA : NB) * W * sizeof(cx<T>)));
         cx<T>* dst = stage0 + (size_t)s * (CF::STAGE / sizeof(cx<T>));
@@ -213,8 +226,7 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
       int pend_isA = -1, pend_g = 0;  // stored, not yet published
       auto publish = [&](int isA, int g) {
         fence_async_global();
-        __threadfence();
-        atomicAdd(isA ? doneA + g : doneB + g, 1u);
+        publish_add(isA ? doneA + g : doneB + g);
       };
       for (unsigned i = 0;; ++i) {
         const int s = i % kFtStages;
@@ -255,7 +267,7 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
   }
 
   // -------------------------------------------------------------- consumers
-  const cx<T>* twN = reinterpret_cast<const cx<T>*>(prm.twN);
+  const cx<T>* twN = s_twN;
   const int b = t % W, tt = t / W;
   for (unsigned i = 0;; ++i) {
     const int s = i % kFtStages;
@@ -274,13 +286,13 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
       for (int u = 0; u < SA::E / SA::RL; ++u)
 #pragma unroll
         for (int m = 0; m < SA::RL; ++m)
-          tw8[u * SA::RL + m] = ldg_cx(twN + ((beta * SA::out_elem(tt, u, m)) & (N - 1)));
+          tw8[u * SA::RL + m] = twN[(beta * SA::out_elem(tt, u, m)) & (N - 1)];
       cx<T> v[SA::E];
 #pragma unroll
       for (int u = 0; u < SA::E / SA::R0; ++u)
 #pragma unroll
         for (int m = 0; m < SA::R0; ++m) v[u * SA::R0 + m] = st[SA::in_elem(tt, u, m) * W + b];
-      STA::run(xbuf, v, tt, b, reinterpret_cast<const cx<T>*>(prm.twA));
+      STA::run(xbuf, v, tt, b, s_twA);
       consumer_bar();  // every thread's stage reads are done before it is overwritten
 #pragma unroll
       for (int u = 0; u < SA::E / SA::RL; ++u)
@@ -303,7 +315,7 @@ fourstep_tma_kernel(const __grid_constant__ CUtensorMap map_in, const __grid_con
       for (int u = 0; u < SB::E / SB::R0; ++u)
 #pragma unroll
         for (int m = 0; m < SB::R0; ++m) v[u * SB::R0 + m] = st[SB::in_elem(tt, u, m) * W + b];
-      STB::run(xbuf, v, tt, b, reinterpret_cast<const cx<T>*>(prm.twB));
+      STB::run(xbuf, v, tt, b, s_twB);
       consumer_bar();
 #pragma unroll
       for (int u = 0; u < SB::E / SB::RL; ++u)

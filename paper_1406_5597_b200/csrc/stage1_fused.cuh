@@ -272,10 +272,7 @@ stage1_fused_kernel(const Stage1Params prm) {
       }
     }
     __syncthreads();
-    if (t == 0) {
-      __threadfence();
-      if (isA) atomicAdd(doneA + plane, 1u);
-    }
+    if (t == 0 && isA) publish_add(doneA + plane);
   }
 }
 
