@@ -215,16 +215,42 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # correctness guard on the timed configuration (reference cli.py:263-271 style)
-    tf.inverse(fp, tf.forward(fp, slab))
-    torch.cuda.synchronize(dev)
-    rt = (torch.linalg.norm(fp.real_out.double() - x.double()) / torch.linalg.norm(x.double())).item()
+    ncomp = 3 if args.config == "turbulence" else 1
     tol = 1e-12 if dt == "float64" else 1e-5
+    if args.config == "turbulence":
+        # BASELINE config 5: 3 velocity components defined in Fourier space
+        # (white-noise phases x k^-5/3 on 1 <= |k| <= 340), batched inverse c2r
+        # then forward r2c.  One step = the batched round trip of all components.
+        specs, reals = [], []
+        for c in range(ncomp):
+            noise = torch.empty_like(x)
+            noise.normal_(generator=gen)
+            buf = torch.empty_like(fp.work1)
+            specs.append(tf.turbulence_spectrum(fp, tf.RealSlab(fp.real_layout, noise), 1.0, 340.0 * n0 / 1024,
+                                                out=buf))
+            reals.append(torch.empty_like(fp.real_out))
+        ref0 = specs[0].data.clone()
+
+        def step():
+            rs = tf.inverse_batch(fp, specs, reals)
+            tf.forward_batch(fp, rs, [s.data for s in specs])
+    else:
+        def step():
+            tf.inverse(fp, tf.forward(fp, slab))
+
+    # correctness guard on the timed configuration (reference cli.py:263-271 style)
+    step()
+    torch.cuda.synchronize(dev)
+    if args.config == "turbulence":
+        rt = (torch.linalg.norm(specs[0].data - ref0) / torch.linalg.norm(ref0)).item()
+        del ref0
+    else:
+        rt = (torch.linalg.norm(fp.real_out.double() - x.double()) / torch.linalg.norm(x.double())).item()
     if not rt <= tol:
         raise SystemExit(f"round-trip check failed: rel L2 {rt:.3e} > {tol}")
 
     for _ in range(args.warmup):
-        tf.inverse(fp, tf.forward(fp, slab))
+        step()
     barrier()
     fp.enable_timing(True)
     fp.reset_instrumentation()
@@ -234,7 +260,7 @@ def run_gpu(args):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            tf.inverse(fp, tf.forward(fp, slab))
+            step()
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -267,14 +293,15 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    flops = pair_flops(n0, n1, n2)
+    flops = pair_flops(n0, n1, n2) * ncomp
     value = flops / (ms * 1e-3) / 1e9
     hbm_peak, peak_kind = peaks()
     hbm, nvl, st3 = algorithmic_bytes(n0, n1, n2, p, s_r)
+    hbm, nvl = hbm * ncomp, nvl * ncomp
     t_roof = max(hbm / (hbm_peak * 1e9), nvl / (NVLINK_GBS * 1e9) if p > 1 else 0.0) * 1e3
     # dominant kernel: the stage-3 strided column c2c (one launch per direction)
-    st3_ms = stages["stage3_us"] / 1e3 / (2 * args.steps)
-    st1_ms = stages["stage1_us"] / 1e3 / (2 * args.steps)
+    st3_ms = stages["stage3_us"] / 1e3 / (2 * args.steps * ncomp)
+    st1_ms = stages["stage1_us"] / 1e3 / (2 * args.steps * ncomp)
     ach = st3 / (st3_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "stage3_traffic.json")
@@ -292,12 +319,15 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "f64" if dt == "float64" else "f32",
         "data": "synthetic: seeded uniform[-1,1) real field generated on device",
         "config": {
-            "workload": f"{n0}x{n1}x{n2} {dt} r2c+c2r pair, slab p={p}",
+            "workload": (f"{n0}x{n1}x{n2} {dt} r2c+c2r pair, slab p={p}" if ncomp == 1 else
+                         f"turbulence: 3 x {n0}x{n1}x{n2} {dt} components, batched inverse c2r then forward r2c, "
+                         f"slab p={p}"),
             "grid": [n0, n1, n2], "p": p, "parallelism": f"slab{p}",
             "l2": f"inputs larger than L2 ({n0p * n1 * n2 * s_r / 1e9:.2f} GB real slab per GPU)",
             "pair_roofline_ms": t_roof, "pair_roofline_frac": t_roof / ms,
-            "stage_ms": {"stage1+1'": st1_ms * 2, "exchange": stages["exchange_us"] / 1e3 / args.steps,
-                         "stage3+3'": st3_ms * 2},
+            "stage_ms_per_pair": {"stage1+1'": st1_ms * 2,
+                                  "exchange": stages["exchange_us"] / 1e3 / (args.steps * ncomp),
+                                  "stage3+3'": st3_ms * 2},
             "roundtrip_rel_l2": rt,
         },
         "roofline": {"bound": "hbm", "kernel": "col_fft_kernel (stage 3 strided n0 c2c)",
@@ -310,7 +340,7 @@ def run_gpu(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "cube":
         gf, _, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
         line["cpu_baseline"] = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
@@ -329,6 +359,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--grid", type=int, default=1024)
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
+    ap.add_argument("--config", choices=["cube", "turbulence"], default="cube",
+                    help="cube: seeded uniform field pair (headline); turbulence: BASELINE config 5")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-planes", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")

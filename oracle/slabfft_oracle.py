@@ -52,6 +52,7 @@ __all__ = [
     "uniform_field",
     "normal_field",
     "stage1_band_staging",
+    "turbulence_amplitude",
 ]
 
 C2R_RESIDUE_TOL = 1e-9  # kernels.py:38
@@ -340,3 +341,17 @@ def uniform_field(shape, seed: int) -> np.ndarray:
 def normal_field(shape, seed: int) -> np.ndarray:
     """iid standard normal from default_rng(seed) (cli.py:78-80)."""
     return np.random.default_rng(seed).standard_normal(shape)
+
+
+def turbulence_amplitude(shape, kmin=1.0, kmax=340.0, exponent=-5.0 / 3.0) -> np.ndarray:
+    """Global (n0, n1, n2c) radial amplitude sqrt(E(|k|) / (4 pi |k|^2)) on the
+    shell kmin <= |k| <= kmax, signed frequencies on axes 0 and 1 (the
+    turbulence configuration of BASELINE.json)."""
+    n0, n1, n2 = shape
+    f0 = np.fft.fftfreq(n0, 1.0 / n0)
+    f1 = np.fft.fftfreq(n1, 1.0 / n1)
+    f2 = np.arange(n2 // 2 + 1, dtype=np.float64)
+    k = np.sqrt(f0[:, None, None] ** 2 + f1[None, :, None] ** 2 + f2[None, None, :] ** 2)
+    shell = (k >= kmin) & (k <= kmax)
+    ks = np.where(shell, k, 1.0)
+    return np.where(shell, np.sqrt(ks ** exponent / (4.0 * np.pi * ks ** 2)), 0.0)
