@@ -272,22 +272,23 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers: HostPairStream copies each
+    # step's real slab host->device, runs the pair and copies the result back;
+    # uploads and downloads of neighbouring steps overlap (PCIe full duplex)
+    if args.config == "turbulence":
+        del specs, reals
     h_in = torch.empty(n0p * n1 * n2, dtype=rdt, pin_memory=True)
     h_in.copy_(x)
     h_out = torch.empty_like(h_in, pin_memory=True)
-    d_in = torch.empty_like(x)
-    barrier()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    tf.inverse(fp, tf.forward(fp, slab))
+    streamer = tf.HostPairStream(fp)
+    streamer.run([h_in], [h_out])  # warm-up
     barrier()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        d_in.copy_(h_in, non_blocking=True)
-        back = tf.inverse(fp, tf.forward(fp, tf.RealSlab(fp.real_layout, d_in)))
-        h_out.copy_(back.data, non_blocking=True)
+    streamer.run([h_in] * e2e_steps, [h_out] * e2e_steps)
     barrier()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    del streamer
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -334,7 +335,8 @@ def run_gpu(args):
                      "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": st3},
-        "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+        "e2e": {"value": pair_flops(n0, n1, n2) / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                "api": "paper_1406_5597_b200.HostPairStream (pinned host slab in, host slab out per step)",
                 "h2d_bytes_per_step": h_in.numel() * h_in.element_size(),
                 "d2h_bytes_per_step": h_out.numel() * h_out.element_size()},
         "gpu_launches": launches,
@@ -361,7 +363,7 @@ def main():
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
     ap.add_argument("--config", choices=["cube", "turbulence"], default="cube",
                     help="cube: seeded uniform field pair (headline); turbulence: BASELINE config 5")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-planes", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

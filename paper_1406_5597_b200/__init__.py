@@ -10,6 +10,7 @@ from .dfft import (DTYPES, FftPlan, forward, gather_real, gather_spectral, inver
 from .errors import (ConfigurationError, ConsistencyError, ContractError, CudaError, LayoutError,
                      ProtocolError, SizeError, SlabFftError, TransportError)
 from .exchange import ExchangeOp, Strategy, exchange_schedule
+from .streaming import HostPairStream
 from .fields import forward_batch, inverse_batch, radial_wavenumber, turbulence_spectrum
 from .layout import (DistAxis, GlobalGrid, RealSlab, SlabLayout, SpectralSlab, SpectralTag,
                      TwoLevelStride, column_stride_descriptor, owned_range, spectral_offset, validate)
