@@ -291,7 +291,7 @@ def scatter_spectral(glob: np.ndarray, p: int) -> list[np.ndarray]:
     outs = []
     for q in range(p):
         band = glob[:, q * n1p : (q + 1) * n1p, :].reshape(p, n0p, n1p, n2c)
-        outs.append(np.ascontiguousarray(band.transpose(1, 0, 2, 3)).reshape(-1))
+        outs.append(band.transpose(1, 0, 2, 3).copy().reshape(-1))  # always a copy: inverse_all consumes it
     return outs
 
 
