@@ -229,13 +229,14 @@ struct Shape {
 // SPLIT (float64) the exchange runs in two rounds of 8-byte words (real parts,
 // then imaginary parts), halving the buffer; otherwise whole complex values.
 // SYNC: 0 = __syncthreads; 32 = __syncwarp (every transform inside one warp);
-// otherwise named barrier 1 over the first SYNC threads (warp-specialised CTAs).
+// otherwise the CTA is split into independent groups of SYNC threads and group
+// g = tid / SYNC synchronises on named barrier 1 + g.
 template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0, bool TWS = false>
 struct Stockham {
   static __device__ __forceinline__ void sync() {
     if constexpr (SYNC == 0) __syncthreads();
     else if constexpr (SYNC == 32) __syncwarp();
-    else asm volatile("bar.sync 1, %0;" ::"n"(SYNC) : "memory");
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / SYNC), "n"(SYNC) : "memory");
   }
   using SH = Shape<L>;
   static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;

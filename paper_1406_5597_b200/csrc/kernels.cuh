@@ -64,6 +64,9 @@ struct RowParams {
 #ifndef TFFFT_PREFETCH
 #define TFFFT_PREFETCH 1
 #endif
+#ifndef TFFFT_COLGROUPS
+#define TFFFT_COLGROUPS 1
+#endif
 // columns per CTA: at least 256 threads, at most 1024 threads and 227 KB of
 // shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
 template <typename T, int L>
@@ -77,6 +80,12 @@ template <typename T, int L> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
   static constexpr int B = col_batch<T, L>();
   static constexpr int THREADS = TPT * B;
+  // The CTA's B columns are split over GROUPS independent thread groups (own
+  // exchange buffer, own named barrier): their smem-exchange and FP64 phases
+  // drift apart and overlap instead of alternating CTA-wide.
+  static constexpr int GROUPS = (B % TFFFT_COLGROUPS == 0 && THREADS / TFFFT_COLGROUPS >= 128) ? TFFFT_COLGROUPS : 1;
+  static constexpr int GB = B / GROUPS;               // columns per group
+  static constexpr int GT = THREADS / GROUPS;         // threads per group
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
   static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
   static constexpr bool SPLIT = sizeof(T) == 8 && TFFFT_SPLIT;
@@ -84,7 +93,7 @@ template <typename T, int L> struct ColCfg {
   static constexpr int QW = 128 / WORD;                          // words per 128 bytes
   // B columns x (QW/B) consecutive threads share one wavefront: offset column b
   // by b*QW/B words so the wavefront covers every bank exactly once
-  static constexpr int S = ((RAW + QW - 1) / QW) * QW + (QW / B > 0 ? QW / B : 1);
+  static constexpr int S = ((RAW + QW - 1) / QW) * QW + (QW / GB > 0 ? QW / GB : 1);
   static constexpr bool XCHG = Shape<L>::P > 1;
   static constexpr size_t P_BYTES = TFFFT_PREFETCH ? sizeof(cx<T>) * THREADS * Shape<L>::E : 0;
   static constexpr size_t X_BYTES = XCHG ? (size_t)WORD * B * S : 0;
@@ -125,16 +134,18 @@ __global__ void __launch_bounds__(ColCfg<T, L>::THREADS)
 col_fft_kernel(const ColParams prm) {
   using CF = ColCfg<T, L>;
   using SH = Shape<L>;
-  using ST = Stockham<T, L, INV, CF::S, CF::PS, CF::SPLIT>;
+  using ST = Stockham<T, L, INV, CF::S, CF::PS, CF::SPLIT, (CF::GROUPS > 1 ? CF::GT : 0)>;
   constexpr int E = SH::E, TPT = SH::TPT, B = CF::B, NT = CF::THREADS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* pf = reinterpret_cast<cx<T>*>(smem_raw);  // [E][NT] prefetch slots
-  void* xs = smem_raw + CF::P_BYTES;               // exchange buffer
   const cx<T>* tw = reinterpret_cast<const cx<T>*>(prm.tw);
 
   const int t = threadIdx.x;
-  const int b = t % B;
-  const int tt = t / B;
+  const int grp = t / CF::GT;              // independent column group
+  const int bl = (t % CF::GT) % CF::GB;    // column within the group
+  const int tt = (t % CF::GT) / CF::GB;    // thread within the column
+  const int b = grp * CF::GB + bl;         // column within the tile
+  void* xs = smem_raw + CF::P_BYTES + (size_t)grp * (CF::X_BYTES / CF::GROUPS);  // group's exchange buffer
   const unsigned is = (unsigned)prm.inner_stride;
   const unsigned bs = (unsigned)prm.block_stride;
   const unsigned ics = (unsigned)prm.ic_shift;
@@ -197,7 +208,7 @@ col_fft_kernel(const ColParams prm) {
       ST::first(v, tt, tw);
       if (nxt < ntiles) next = column(nxt);
     }
-    ST::finish(xs, v, tt, b, tw);
+    ST::finish(xs, v, tt, bl, tw);
 
     if (cur.valid) {
       if constexpr (REDIR) {
@@ -302,39 +313,36 @@ c2r_rows_kernel(const RowParams prm) {
   const bool valid = row < prm.nrows;
   const cx<T>* in = reinterpret_cast<const cx<T>*>(prm.spec) + (valid ? row : 0) * prm.n2c;
 
-  double m2 = 0.0, edge = 0.0, resid = 0.0;
+  // row -> shared memory, with the statistics of the Hermitian check: max |X|^2
+  // over the row (every thread), |Im X_0|, |Im X_N| (thread tt == 0 only)
+  double m2 = 0.0;
 #pragma unroll
-  for (int q = 0; q <= SH::E; ++q) {
+  for (int q = 0; q < SH::E; ++q) {
     const int k = tt + SH::TPT * q;
-    if (k <= N && (q < SH::E || tt == 0)) {
-      cx<T> X = valid ? in[k] : cx<T>{T(0), T(0)};
-      const double a2 = (double)X.x * X.x + (double)X.y * X.y;
-      m2 = fmax(m2, a2);
-      if (k == 0 || k == N) {
-        const double im = fabs((double)X.y);
-        edge = fmax(edge, im);
-        resid += im;
-        X.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
-      }
-      sm[ST::sidx(b, k)] = X;
-    }
+    const cx<T> X = in[k];
+    m2 = fmax(m2, fma((double)X.x, (double)X.x, (double)X.y * X.y));
+    sm[ST::sidx(b, k)] = X;
   }
-  // statistics: reduce over the TPT threads of this row, one atomic per row-warp
+  if (tt == 0) {
+    cx<T> X0 = sm[ST::sidx(b, 0)];
+    cx<T> XN = in[N];
+    m2 = fmax(m2, fma((double)XN.x, (double)XN.x, (double)XN.y * XN.y));
+    const double e0 = fabs((double)X0.y), eN = fabs((double)XN.y);
+    if (valid && prm.stats != nullptr) {
+      unsigned long long* st = prm.stats + 3 * (row / prm.rows_per_plane);
+      atomicMax(st + 1, ord(fmax(e0, eN)));
+      atomicMax(st + 2, ord(e0 + eN));
+    }
+    X0.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
+    XN.y = T(0);
+    sm[ST::sidx(b, 0)] = X0;
+    sm[ST::sidx(b, N)] = XN;
+  }
   constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
 #pragma unroll
-  for (int o = W / 2; o > 0; o >>= 1) {
-    m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o, W));
-    edge = fmax(edge, __shfl_xor_sync(0xffffffffu, edge, o, W));
-    resid += __shfl_xor_sync(0xffffffffu, resid, o, W);
-  }
-  if (valid && prm.stats != nullptr && (tt % W) == 0) {
-    unsigned long long* st = prm.stats + 3 * (row / prm.rows_per_plane);
-    atomicMax(st + 0, ord(m2));
-    if (tt == 0) {
-      atomicMax(st + 1, ord(edge));
-      atomicMax(st + 2, ord(resid));
-    }
-  }
+  for (int o = W / 2; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o, W));
+  if (valid && prm.stats != nullptr && (tt % W) == 0)
+    atomicMax(prm.stats + 3 * (row / prm.rows_per_plane), ord(m2));
   __syncthreads();
 
   cx<T> v[SH::E];
