@@ -69,11 +69,13 @@ struct RowParams {
 #endif
 // columns per CTA: at least 256 threads, at most 1024 threads and 227 KB of
 // shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
+// (float64: 8 columns = 128-byte row visits; float32: 16 columns = 128 bytes)
 template <typename T, int L>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
-  int b = 256 / TPT > TFFFT_COLB ? 256 / TPT : TFFFT_COLB;
-  while (b > 1 && (TPT * b > 1024 || (size_t)b * N * (sizeof(cx<T>) + 8) + 4096 > 227 * 1024)) b /= 2;
+  constexpr int want = TFFFT_COLB * (int)(16 / sizeof(cx<T>));
+  int b = 256 / TPT > want ? 256 / TPT : want;
+  while (b > 1 && (TPT * b > 1024 || (size_t)b * N * (sizeof(cx<T>) + sizeof(T)) + 4096 > 227 * 1024)) b /= 2;
   return b;
 }
 template <typename T, int L> struct ColCfg {
@@ -88,8 +90,9 @@ template <typename T, int L> struct ColCfg {
   static constexpr int GT = THREADS / GROUPS;         // threads per group
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;
   static constexpr int RAW = Shape<L>::N + (Shape<L>::N >> (PS > 20 ? 30 : PS));
-  static constexpr bool SPLIT = sizeof(T) == 8 && TFFFT_SPLIT;
-  static constexpr int WORD = SPLIT ? 8 : (int)sizeof(cx<T>);  // exchange word bytes
+  // exchange in real-valued words (re round, then im round): halves the buffer
+  static constexpr bool SPLIT = TFFFT_SPLIT;
+  static constexpr int WORD = SPLIT ? (int)sizeof(T) : (int)sizeof(cx<T>);  // exchange word bytes
   static constexpr int QW = 128 / WORD;                          // words per 128 bytes
   // B columns x (QW/B) consecutive threads share one wavefront: offset column b
   // by b*QW/B words so the wavefront covers every bank exactly once
