@@ -69,18 +69,19 @@ struct RowParams {
 #endif
 // columns per CTA: at least 256 threads, at most 1024 threads and 227 KB of
 // shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
-// (float64: 8 columns = 128-byte row visits; float32: 16 columns = 128 bytes)
-template <typename T, int L>
+// WIDE (stage 3, rows megabytes apart): 128-byte row visits, i.e. 8 float64 or
+// 16 float32 columns; otherwise 8 columns
+template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
-  constexpr int want = TFFFT_COLB * (int)(16 / sizeof(cx<T>));
+  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_COLB;
   int b = 256 / TPT > want ? 256 / TPT : want;
   while (b > 1 && (TPT * b > 1024 || (size_t)b * N * (sizeof(cx<T>) + sizeof(T)) + 4096 > 227 * 1024)) b /= 2;
   return b;
 }
-template <typename T, int L> struct ColCfg {
+template <typename T, int L, bool WIDE = false> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
-  static constexpr int B = col_batch<T, L>();
+  static constexpr int B = col_batch<T, L, WIDE>();
   static constexpr int THREADS = TPT * B;
   // The CTA's B columns are split over GROUPS independent thread groups (own
   // exchange buffer, own named barrier): their smem-exchange and FP64 phases
@@ -111,9 +112,9 @@ template <int L> struct RowCfg {
   static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
 };
 
-template <typename T, int L>
+template <typename T, int L, bool WIDE = false>
 __host__ __device__ constexpr size_t col_smem_bytes() {
-  return ColCfg<T, L>::P_BYTES + ColCfg<T, L>::X_BYTES;
+  return ColCfg<T, L, WIDE>::P_BYTES + ColCfg<T, L, WIDE>::X_BYTES;
 }
 template <typename T, int L>
 __host__ __device__ constexpr size_t row_smem_bytes() {
@@ -132,10 +133,10 @@ __host__ __device__ constexpr size_t row_smem_bytes() {
 // REDIR : epilogue sends peer bands to the exchange staging buffer.
 // All element offsets are 32-bit (plan_create bounds the slab below 2^32
 // elements); the 64-bit column base pointer is formed once per tile.
-template <typename T, int L, bool INV, bool TWO, bool REDIR>
-__global__ void __launch_bounds__(ColCfg<T, L>::THREADS)
+template <typename T, int L, bool INV, bool TWO, bool REDIR, bool WIDE>
+__global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS)
 col_fft_kernel(const ColParams prm) {
-  using CF = ColCfg<T, L>;
+  using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
   using ST = Stockham<T, L, INV, CF::S, CF::PS, CF::SPLIT, (CF::GROUPS > 1 ? CF::GT : 0)>;
   constexpr int E = SH::E, TPT = SH::TPT, B = CF::B, NT = CF::THREADS;
@@ -380,8 +381,9 @@ c2r_rows_kernel(const RowParams prm) {
 
 // host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)
 // variant: 0 = single stride, 1 = single stride + redirect, 2 = two-level, 3 = two-level + redirect
+// wide: stage-3 tiles (128-byte row visits for either precision)
 template <typename T>
-cudaError_t launch_col_fft(int L, bool inv, int variant, const ColParams& p, cudaStream_t s);
+cudaError_t launch_col_fft(int L, bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_r2c_rows(int L, const RowParams& p, cudaStream_t s);
 template <typename T>

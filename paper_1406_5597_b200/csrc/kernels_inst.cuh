@@ -25,11 +25,11 @@ static int num_sms() {
   return n;
 }
 
-template <typename T, int L, bool INV, bool TWO, bool REDIR>
+template <typename T, int L, bool INV, bool TWO, bool REDIR, bool WIDE>
 static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
-  using CF = ColCfg<T, L>;
-  const size_t sm = col_smem_bytes<T, L>();
-  auto k = col_fft_kernel<T, L, INV, TWO, REDIR>;
+  using CF = ColCfg<T, L, WIDE>;
+  const size_t sm = col_smem_bytes<T, L, WIDE>();
+  auto k = col_fft_kernel<T, L, INV, TWO, REDIR, WIDE>;
   static cudaError_t prep = prep_smem(k, sm);
   if (prep != cudaSuccess) return prep;
   static int per_sm = [&] {
@@ -80,28 +80,28 @@ static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
 // instantiated variants: stage 1b fwd (+redirect), stage 1b' inv, stage 3 fwd
 // (single / two-level), stage 3' inv (single / two-level + redirect)
 template <typename T, int L>
-static cudaError_t col_dispatch(bool inv, int variant, const ColParams& p, cudaStream_t s) {
-  if (!inv) {
-    switch (variant) {
-      case 0: return col_one<T, L, false, false, false>(p, s);
-      case 1: return col_one<T, L, false, false, true>(p, s);
-      case 2: return col_one<T, L, false, true, false>(p, s);
-      default: return cudaErrorInvalidValue;
-    }
+static cudaError_t col_dispatch(bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s) {
+  // stage 1b / 1b' (narrow): fwd 0 / 1 (redirect), inv 0
+  // stage 3 / 3' (wide): fwd 0 / 2 (two-level), inv 0 / 3 (two-level + redirect)
+  if (!wide) {
+    if (!inv && variant == 0) return col_one<T, L, false, false, false, false>(p, s);
+    if (!inv && variant == 1) return col_one<T, L, false, false, true, false>(p, s);
+    if (inv && variant == 0) return col_one<T, L, true, false, false, false>(p, s);
+    return cudaErrorInvalidValue;
   }
-  switch (variant) {
-    case 0: return col_one<T, L, true, false, false>(p, s);
-    case 3: return col_one<T, L, true, true, true>(p, s);
-    default: return cudaErrorInvalidValue;
-  }
+  if (!inv && variant == 0) return col_one<T, L, false, false, false, true>(p, s);
+  if (!inv && variant == 2) return col_one<T, L, false, true, false, true>(p, s);
+  if (inv && variant == 0) return col_one<T, L, true, false, false, true>(p, s);
+  if (inv && variant == 3) return col_one<T, L, true, true, true, true>(p, s);
+  return cudaErrorInvalidValue;
 }
 #define TFFFT_COL_CASE(LL) \
-  case LL: return col_dispatch<TFFFT_REAL, LL>(inv, variant, p, s);
+  case LL: return col_dispatch<TFFFT_REAL, LL>(inv, variant, wide, p, s);
 #define TFFFT_ROW_CASE(LL, FN) \
   case LL: return FN<TFFFT_REAL, LL>(p, s);
 
 template <>
-cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, int variant, const ColParams& p, cudaStream_t s) {
+cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s) {
   switch (L) {
     TFFFT_COL_CASE(1) TFFFT_COL_CASE(2) TFFFT_COL_CASE(3) TFFFT_COL_CASE(4)
     TFFFT_COL_CASE(5) TFFFT_COL_CASE(6) TFFFT_COL_CASE(7) TFFFT_COL_CASE(8)

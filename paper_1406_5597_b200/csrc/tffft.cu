@@ -285,11 +285,11 @@ static int upload_table(const std::vector<double>& t, int dtype, void** dev, siz
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 // ---------------------------------------------------------------------------
-static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, int variant, const ColParams& prm,
+static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, int variant, bool wide, const ColParams& prm,
                               cudaStream_t s) {
   pl->launches++;
-  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, variant, prm, s)
-                                : launch_col_fft<float>(L, inv, variant, prm, s);
+  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, variant, wide, prm, s)
+                                : launch_col_fft<float>(L, inv, variant, wide, prm, s);
 }
 static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
@@ -338,7 +338,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
   }
-  CUDA_TRY(col_launch(pl, pl->L1, inv, c.staging ? 1 : 0, c, s));
+  CUDA_TRY(col_launch(pl, pl->L1, inv, c.staging ? 1 : 0, false, c, s));
   return TFFFT_OK;
 }
 
@@ -479,7 +479,7 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.stg_within = (long long)pl->n1p * pl->n2c;
     c.stg_grp = 0;
   }
-  CUDA_TRY(col_launch(pl, pl->L0, inv, pl->p == 1 ? 0 : (c.staging ? 3 : 2), c, s));
+  CUDA_TRY(col_launch(pl, pl->L0, inv, pl->p == 1 ? 0 : (c.staging ? 3 : 2), true, c, s));
   return TFFFT_OK;
 }
 
