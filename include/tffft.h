@@ -118,9 +118,11 @@ int tffft_launch_count(tffft_plan_t plan, uint64_t* launches);
 
 /* --- host-only geometry (no GPU needed) ---------------------------------- */
 /* STRIDED exchange schedule of one rank: up to max_ops rows of
- * {peer, send_offset, recv_offset, count} in complex elements, where
- * send_offset indexes the staging buffer [q][i][j][k] and recv_offset the
- * spectral slab.  Same list for forward and inverse (exchange.py:120-121). */
+ * {peer, send_offset, recv_offset, count} in complex elements: one send of the
+ * staging band [q][i][j][k] and one receive into the landing band, per peer.
+ * The FFT stage after the exchange reads the landing band through the
+ * STRIDED_INPLACE addressing (exchange.py:114-121's strided descriptor applied
+ * by the kernel).  Same list for forward and inverse (exchange.py:120-121). */
 int tffft_exchange_schedule(int n0, int n1, int n2, int p, int rank, int64_t* ops, int64_t max_ops,
                             int64_t* nops);
 /* twiddle-table geometry of the radix schedule for length 2^log2n (for tests) */

@@ -21,7 +21,7 @@ namespace tffft {
 //   -> staging + band*stg_band + (e & band_mask)*stg_within + (c / cpb)*stg_grp + (c % cpb)
 struct ColParams {
   void* data;
-  void* staging;
+  void* staging;          // RD == 1: peer bands written here; RD == 2: peer bands read from here (landing)
   const void* tw;
   long long ncols;
   int cpb;
@@ -130,10 +130,16 @@ __host__ __device__ constexpr size_t row_smem_bytes() {
 // will feed into pass 0, so the hand-off needs no CTA barrier.
 // TWO   : element offsets use the two-level STRIDED_INPLACE formula (p > 1,
 //         stage 3); otherwise offset = e * inner_stride.
-// REDIR : epilogue sends peer bands to the exchange staging buffer.
+// RD    : 0 = in place; 1 = the epilogue writes peer bands to the exchange
+//         staging buffer; 2 = peer bands are READ from the exchange landing
+//         buffer (where the exchange delivered them contiguously) and every
+//         element is written in place -- the strided "datatype" of the
+//         reference's exchange (exchange.py:114-121) applied by the FFT's own
+//         addressing, with no rearrangement pass.  Staging and landing share the
+//         [band][i][j][k] chunk layout described by stg_band/stg_within/stg_grp.
 // All element offsets are 32-bit (plan_create bounds the slab below 2^32
 // elements); the 64-bit column base pointer is formed once per tile.
-template <typename T, int L, bool INV, bool TWO, bool REDIR, bool WIDE>
+template <typename T, int L, bool INV, bool TWO, int RD, bool WIDE>
 __global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS)
 col_fft_kernel(const ColParams prm) {
   using CF = ColCfg<T, L, WIDE>;
@@ -169,9 +175,19 @@ col_fft_kernel(const ColParams prm) {
     const unsigned cr = c - cq * (unsigned)prm.cpb;
     return {reinterpret_cast<cx<T>*>(prm.data) + ((long long)cq * prm.grp_stride + cr), cq, cr, valid};
   };
+  const unsigned bmask = (1u << prm.band_shift) - 1u;
+  auto src = [&](const Col& col, unsigned e) -> const cx<T>* {
+    if constexpr (RD == 2) {
+      const int band = (int)(e >> prm.band_shift);
+      if (band != prm.self_band)
+        return reinterpret_cast<const cx<T>*>(prm.staging) + ((long long)col.cq * prm.stg_grp + col.cr) +
+               (long long)band * prm.stg_band + (long long)(e & bmask) * prm.stg_within;
+    }
+    return col.p + offset(e);
+  };
   auto prefetch = [&](const Col& col) {
 #pragma unroll
-    for (int kk = 0; kk < E; ++kk) cp_async<sizeof(cx<T>)>(pf + kk * NT + t, col.p + offset(tt + TPT * kk));
+    for (int kk = 0; kk < E; ++kk) cp_async<sizeof(cx<T>)>(pf + kk * NT + t, src(col, tt + TPT * kk));
     cp_commit();
   };
 
@@ -208,16 +224,15 @@ col_fft_kernel(const ColParams prm) {
       }
     } else {
 #pragma unroll
-      for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = cur.p[offset(tt + TPT * kk)];
+      for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = *src(cur, tt + TPT * kk);
       ST::first(v, tt, tw);
       if (nxt < ntiles) next = column(nxt);
     }
     ST::finish(xs, v, tt, bl, tw);
 
     if (cur.valid) {
-      if constexpr (REDIR) {
+      if constexpr (RD == 1) {
         cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging) + ((long long)cur.cq * prm.stg_grp + cur.cr);
-        const unsigned bmask = (1u << prm.band_shift) - 1u;
         const unsigned sb = (unsigned)prm.stg_band, sw = (unsigned)prm.stg_within;
 #pragma unroll
         for (int u = 0; u < E / SH::RL; ++u)
@@ -381,9 +396,10 @@ c2r_rows_kernel(const RowParams prm) {
 
 // host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)
 // variant: 0 = single stride, 1 = single stride + redirect, 2 = two-level, 3 = two-level + redirect
-// wide: stage-3 tiles (128-byte row visits for either precision)
+// wide: stage-3 tiles (128-byte row visits for either precision); two: two-level
+// element offsets; rd: 0 in place, 1 write peer bands to staging, 2 read peer bands from landing
 template <typename T>
-cudaError_t launch_col_fft(int L, bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s);
+cudaError_t launch_col_fft(int L, bool inv, bool two, int rd, bool wide, const ColParams& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_r2c_rows(int L, const RowParams& p, cudaStream_t s);
 template <typename T>

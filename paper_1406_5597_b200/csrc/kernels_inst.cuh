@@ -25,11 +25,11 @@ static int num_sms() {
   return n;
 }
 
-template <typename T, int L, bool INV, bool TWO, bool REDIR, bool WIDE>
+template <typename T, int L, bool INV, bool TWO, int RD, bool WIDE>
 static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   using CF = ColCfg<T, L, WIDE>;
   const size_t sm = col_smem_bytes<T, L, WIDE>();
-  auto k = col_fft_kernel<T, L, INV, TWO, REDIR, WIDE>;
+  auto k = col_fft_kernel<T, L, INV, TWO, RD, WIDE>;
   static cudaError_t prep = prep_smem(k, sm);
   if (prep != cudaSuccess) return prep;
   static int per_sm = [&] {
@@ -80,28 +80,33 @@ static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
 // instantiated variants: stage 1b fwd (+redirect), stage 1b' inv, stage 3 fwd
 // (single / two-level), stage 3' inv (single / two-level + redirect)
 template <typename T, int L>
-static cudaError_t col_dispatch(bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s) {
-  // stage 1b / 1b' (narrow): fwd 0 / 1 (redirect), inv 0
-  // stage 3 / 3' (wide): fwd 0 / 2 (two-level), inv 0 / 3 (two-level + redirect)
+static cudaError_t col_dispatch(bool inv, bool two, int rd, bool wide, const ColParams& p, cudaStream_t s) {
+  // stage 1b (narrow): forward in place / + peer bands to staging (p > 1)
+  //          1b':      inverse in place / + peer bands read from landing (p > 1)
+  // stage 3  (wide):   forward in place (p = 1) / two-level + landing reads (p > 1)
+  //          3':       inverse in place (p = 1) / two-level + staging writes (p > 1)
   if (!wide) {
-    if (!inv && variant == 0) return col_one<T, L, false, false, false, false>(p, s);
-    if (!inv && variant == 1) return col_one<T, L, false, false, true, false>(p, s);
-    if (inv && variant == 0) return col_one<T, L, true, false, false, false>(p, s);
+    if (two) return cudaErrorInvalidValue;
+    if (!inv && rd == 0) return col_one<T, L, false, false, 0, false>(p, s);
+    if (!inv && rd == 1) return col_one<T, L, false, false, 1, false>(p, s);
+    if (inv && rd == 0) return col_one<T, L, true, false, 0, false>(p, s);
+    if (inv && rd == 2) return col_one<T, L, true, false, 2, false>(p, s);
     return cudaErrorInvalidValue;
   }
-  if (!inv && variant == 0) return col_one<T, L, false, false, false, true>(p, s);
-  if (!inv && variant == 2) return col_one<T, L, false, true, false, true>(p, s);
-  if (inv && variant == 0) return col_one<T, L, true, false, false, true>(p, s);
-  if (inv && variant == 3) return col_one<T, L, true, true, true, true>(p, s);
+  if (!inv && !two && rd == 0) return col_one<T, L, false, false, 0, true>(p, s);
+  if (!inv && two && rd == 2) return col_one<T, L, false, true, 2, true>(p, s);
+  if (inv && !two && rd == 0) return col_one<T, L, true, false, 0, true>(p, s);
+  if (inv && two && rd == 1) return col_one<T, L, true, true, 1, true>(p, s);
   return cudaErrorInvalidValue;
 }
 #define TFFFT_COL_CASE(LL) \
-  case LL: return col_dispatch<TFFFT_REAL, LL>(inv, variant, wide, p, s);
+  case LL: return col_dispatch<TFFFT_REAL, LL>(inv, two, rd, wide, p, s);
 #define TFFFT_ROW_CASE(LL, FN) \
   case LL: return FN<TFFFT_REAL, LL>(p, s);
 
 template <>
-cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, int variant, bool wide, const ColParams& p, cudaStream_t s) {
+cudaError_t launch_col_fft<TFFFT_REAL>(int L, bool inv, bool two, int rd, bool wide, const ColParams& p,
+                                       cudaStream_t s) {
   switch (L) {
     TFFFT_COL_CASE(1) TFFFT_COL_CASE(2) TFFFT_COL_CASE(3) TFFFT_COL_CASE(4)
     TFFFT_COL_CASE(5) TFFFT_COL_CASE(6) TFFFT_COL_CASE(7) TFFFT_COL_CASE(8)

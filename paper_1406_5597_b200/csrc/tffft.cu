@@ -197,7 +197,8 @@ struct tffft_plan_s {
   int n0p = 0, n1p = 0, n2c = 0;
   size_t esz = 16;  // complex element bytes
   int seq = 0;
-  void* staging = nullptr;
+  void* staging = nullptr;   // outgoing peer bands [q][i][j][k]
+  void* landing = nullptr;   // incoming peer bands [q][i][j][k]
   void* tw0 = nullptr;
   void* tw1 = nullptr;
   void* tw2 = nullptr;
@@ -285,11 +286,11 @@ static int upload_table(const std::vector<double>& t, int dtype, void** dev, siz
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 // ---------------------------------------------------------------------------
-static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, int variant, bool wide, const ColParams& prm,
+static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd, bool wide, const ColParams& prm,
                               cudaStream_t s) {
   pl->launches++;
-  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, variant, wide, prm, s)
-                                : launch_col_fft<float>(L, inv, variant, wide, prm, s);
+  return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, two, rd, wide, prm, s)
+                                : launch_col_fft<float>(L, inv, two, rd, wide, prm, s);
 }
 static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
@@ -331,14 +332,17 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   c.band_shift = ilog2(pl->n1p);
   c.self_band = pl->rank;
   c.staging = nullptr;
-  if (!inv && pl->p > 1) {
-    // forward epilogue: band q != rank -> staging[q][i][j][k]
-    c.staging = pl->staging;
+  int rd = 0;
+  if (pl->p > 1) {
+    // forward epilogue: band q != rank -> staging[q][i][j][k];
+    // inverse: band q != rank is read from landing[q][i][j][k] (the exchange output)
+    c.staging = inv ? pl->landing : pl->staging;
+    rd = inv ? 2 : 1;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
   }
-  CUDA_TRY(col_launch(pl, pl->L1, inv, c.staging ? 1 : 0, false, c, s));
+  CUDA_TRY(col_launch(pl, pl->L1, inv, false, rd, false, c, s));
   return TFFFT_OK;
 }
 
@@ -472,14 +476,17 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.pf_ahead = aligned ? ahead : 0;
     c.pf_bytes = pfb;
   }
-  if (inv && pl->p > 1) {
+  int rd = 0;
+  if (pl->p > 1) {
+    // forward: block s != rank is read from landing[s][i][c] (the exchange output);
     // inverse epilogue: block s != rank -> staging[s][i][c]
-    c.staging = pl->staging;
+    c.staging = inv ? pl->staging : pl->landing;
+    rd = inv ? 1 : 2;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = (long long)pl->n1p * pl->n2c;
     c.stg_grp = 0;
   }
-  CUDA_TRY(col_launch(pl, pl->L0, inv, pl->p == 1 ? 0 : (c.staging ? 3 : 2), true, c, s));
+  CUDA_TRY(col_launch(pl, pl->L0, inv, pl->p > 1, rd, true, c, s));
   return TFFFT_OK;
 }
 
@@ -542,24 +549,25 @@ static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
   return TFFFT_OK;
 }
 
-// the exchange proper: staging[q][i] -> peer q's spectral slab at band rank of plane i
+// The exchange proper (exchange.py:263-290): my staging band q (n0p chunks of
+// (n1/p)*n2c, contiguous) goes to rank q, whose landing band for me receives
+// it; the next FFT stage reads the landing buffer through the STRIDED_INPLACE
+// addressing, so no rearrangement pass follows.  One send and one receive per
+// peer (the reference posts one strided LayoutDescriptor per peer).
 static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  (void)spec;
   if (pl->p == 1) return TFFFT_OK;
-  const long long chunk = (long long)pl->n1p * pl->n2c;  // complex elements
+  const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
   if (pl->comm->is_nccl) {
     NcclApi& api = nccl();
     const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
     char* stg = static_cast<char*>(pl->staging);
-    char* dst = static_cast<char*>(spec);
+    char* lnd = static_cast<char*>(pl->landing);
     NCCL_TRY(api.GroupStart());
     for (int d = 1; d < pl->p; ++d) {
       const int to = (pl->rank + d) % pl->p, from = (pl->rank - d + pl->p) % pl->p;
-      for (int i = 0; i < pl->n0p; ++i) {
-        NCCL_TRY(api.Send(stg + ((long long)to * pl->n0p + i) * chunk * pl->esz, 2 * chunk, dt, to,
-                          pl->comm->nccl, s));
-        NCCL_TRY(api.Recv(dst + ((long long)i * pl->n1 * pl->n2c + (long long)from * chunk) * pl->esz,
-                          2 * chunk, dt, from, pl->comm->nccl, s));
-      }
+      NCCL_TRY(api.Send(stg + (long long)to * band * pl->esz, 2 * band, dt, to, pl->comm->nccl, s));
+      NCCL_TRY(api.Recv(lnd + (long long)from * band * pl->esz, 2 * band, dt, from, pl->comm->nccl, s));
     }
     NCCL_TRY(api.GroupEnd());
   } else {
@@ -569,12 +577,12 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
     TRY(fab.barrier());
     for (int q = 0; q < pl->p; ++q)
       if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.ready[q], 0));
-    // 16-byte words when every chunk (and so every chunk offset) is a multiple of 16 bytes
-    const long long bytes = chunk * (long long)pl->esz;
-    const bool wide = bytes % 16 == 0 && reinterpret_cast<uintptr_t>(spec) % 16 == 0;
+    // pull: landing[q] <- staging_q[rank], one band per peer
+    const long long bytes = band * (long long)pl->esz;
+    const bool wide = bytes % 16 == 0;
     const long long words = wide ? bytes / 16 : bytes / 8;
-    const int nchunks = (pl->p - 1) * pl->n0p;
-    dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 64), (unsigned)nchunks);
+    const int nchunks = pl->p - 1;
+    dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 2048), (unsigned)nchunks);
     if (wide)
       pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(pl->pull_ptrs, words, nchunks);
     else
@@ -599,23 +607,18 @@ static int fabric_setup(tffft_plan_t pl, void* /*unused*/) {
   return TFFFT_OK;
 }
 
-// the pull list depends on the destination spectral buffer: (re)built per call
-static int fabric_pull_list(tffft_plan_t pl, void* spec, cudaStream_t s) {
+// pull list of the local fabric: (peer q's staging band for me, my landing band q)
+static int fabric_pull_list(tffft_plan_t pl) {
   LocalFabric& fab = *pl->comm->fabric;
   auto& slot = fab.slot(pl->seq);
-  const long long chunk = (long long)pl->n1p * pl->n2c;
+  const long long band = (long long)pl->n0p * pl->n1p * pl->n2c * (long long)pl->esz;
   std::vector<void*> h;
-  h.reserve(2 * (size_t)(pl->p - 1) * pl->n0p);
   for (int q = 0; q < pl->p; ++q) {
     if (q == pl->rank) continue;
-    char* src = static_cast<char*>(slot.staging[q]);
-    for (int i = 0; i < pl->n0p; ++i) {
-      h.push_back(src + ((long long)pl->rank * pl->n0p + i) * chunk * pl->esz);
-      h.push_back(static_cast<char*>(spec) + ((long long)i * pl->n1 * pl->n2c + (long long)q * chunk) * pl->esz);
-    }
+    h.push_back(static_cast<char*>(slot.staging[q]) + (long long)pl->rank * band);
+    h.push_back(static_cast<char*>(pl->landing) + (long long)q * band);
   }
-  CUDA_TRY(cudaMemcpyAsync(pl->pull_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
-  // the pageable copy above is synchronous w.r.t. the host buffer, so h may go out of scope
+  CUDA_TRY(cudaMemcpy(pl->pull_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice));
   return TFFFT_OK;
 }
 
@@ -770,13 +773,15 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   if (p > 1) {
     const size_t sb = (size_t)p * pl->n0p * pl->n1p * pl->n2c * pl->esz;
     CUDA_TRY(cudaMalloc(&pl->staging, sb));
-    ws += sb;
+    CUDA_TRY(cudaMalloc(&pl->landing, sb));
+    ws += 2 * sb;
     if (!comm->is_nccl) {
-      const size_t nptr = 2 * (size_t)(p - 1) * pl->n0p;
+      const size_t nptr = 2 * (size_t)(p - 1);
       CUDA_TRY(cudaMalloc(&pl->pull_ptrs, nptr * sizeof(void*)));
       ws += nptr * sizeof(void*);
       pl->seq = comm->plan_seq++;
       TRY(fabric_setup(pl.get(), nullptr));
+      TRY(fabric_pull_list(pl.get()));
     }
   }
   // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
@@ -785,7 +790,8 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // algorithmic bytes with 1 KB row visits but issues ~60% more instructions per
     // element than the direct 8-column kernel, which is faster today; opt-in
     // with TFFFT_FOURSTEP=1.
-    const int la = (flags & TFFFT_FLAG_FOURSTEP_STAGE3) ? fourstep_la(pl->L0) : 0;
+    // optional schedules are single-rank kernels (no staging / landing addressing)
+    const int la = ((flags & TFFFT_FLAG_FOURSTEP_STAGE3) && p == 1) ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
       const long long ncols = (long long)pl->n1p * pl->n2c;
@@ -808,7 +814,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // measured at 1024^3 (profiles/r01_*): the fused persistent stage 1 keeps the
     // planes in L2 but its mixed row/column tasks run at lower occupancy; the two
     // streaming kernels are faster today, so fusion is opt-in (TFFFT_FUSE=1)
-    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && stage1_fused_supported(pl->L2h, pl->L1)) {
+    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && p == 1 && stage1_fused_supported(pl->L2h, pl->L1)) {
       pl->s1_fused = true;
       CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
@@ -843,7 +849,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaSetDevice(pl->comm->device);
   free_events(pl);
   cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
-  cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->pull_ptrs);
+  cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
@@ -891,7 +897,6 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
   }
   MARK(ev, 1, s);
   // exchange (exchange.py:263-276)
-  if (pl->p > 1 && !pl->comm->is_nccl) TRY(fabric_pull_list(pl, spec_out, s));
   TRY(exchange(pl, spec_out, s));
   MARK(ev, 2, s);
   // stage 3: strided columns (dfft.py:170-171)
@@ -914,7 +919,6 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   TRY(stage3_columns(pl, spec, true, s));
   MARK(ev, 1, s);
   // exchange (exchange.py:279-290)
-  if (pl->p > 1 && !pl->comm->is_nccl) TRY(fabric_pull_list(pl, spec, s));
   TRY(exchange(pl, spec, s));
   MARK(ev, 2, s);
   // stage 1' (dfft.py:206-209)
@@ -1010,19 +1014,17 @@ int tffft_exchange_schedule(int n0, int n1, int n2, int p, int rank, int64_t* op
   if (!nops) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   if (p < 1 || rank < 0 || rank >= p || n0 % p || n1 % p)
     return fail(TFFFT_ERR_CONFIGURATION, "invalid geometry");
-  const int64_t n0p = n0 / p, n1p = n1 / p, n2c = n2 / 2 + 1, chunk = n1p * n2c;
+  const int64_t n0p = n0 / p, n1p = n1 / p, n2c = n2 / 2 + 1, band = n0p * n1p * n2c;
   int64_t cnt = 0;
   for (int d = 1; d < p; ++d) {
     const int q = (rank + d) % p;
-    for (int64_t i = 0; i < n0p; ++i) {
-      if (ops && cnt < max_ops) {
-        ops[4 * cnt + 0] = q;
-        ops[4 * cnt + 1] = ((int64_t)q * n0p + i) * chunk;        // staging[q][i]
-        ops[4 * cnt + 2] = i * n1 * n2c + (int64_t)q * chunk;      // spectral band q of plane i
-        ops[4 * cnt + 3] = chunk;
-      }
-      ++cnt;
+    if (ops && cnt < max_ops) {
+      ops[4 * cnt + 0] = q;
+      ops[4 * cnt + 1] = (int64_t)q * band;  // staging[q]: my planes' band q, [i][j][k]
+      ops[4 * cnt + 2] = (int64_t)q * band;  // landing[q]: rank q's planes' band rank, [i][j][k]
+      ops[4 * cnt + 3] = band;
     }
+    ++cnt;
   }
   *nops = cnt;
   if (ops && cnt > max_ops) return fail(TFFFT_ERR_CONFIGURATION, "ops buffer too small (%lld needed)", (long long)cnt);

@@ -25,11 +25,13 @@ class Strategy(Enum):
 
 @dataclass(frozen=True)
 class ExchangeOp:
-    """One chunk of the STRIDED exchange: ``count`` complex elements go from
-    staging[send_offset] to peer's spectral slab, and the matching chunk from
-    that peer lands at spectral[recv_offset].  The chunk is one block of the
-    reference's LayoutDescriptor(count=n0/p, block_length=(n1/p)*n2c,
-    stride=n1*n2c, base=q*(n1/p)*n2c) (exchange.py:114-119)."""
+    """One peer of the STRIDED exchange: ``count`` complex elements (the
+    n0/p chunks of (n1/p)*n2c of the reference's LayoutDescriptor(count=n0/p,
+    block_length=(n1/p)*n2c, stride=n1*n2c, base=q*(n1/p)*n2c),
+    exchange.py:114-119) go from staging[send_offset] to the peer, and the
+    peer's band for this rank arrives at landing[recv_offset].  The FFT stage
+    after the exchange reads the landing band through the STRIDED_INPLACE
+    addressing, so no rearrangement pass follows."""
 
     peer: int
     send_offset: int

@@ -1,8 +1,10 @@
 """Multi-rank host path on CPU (gloo, world_size 2 and 4): each rank takes
 the oracle's stage-1 output, splits it the way the GPU stage-1 epilogue does
-(self band in place, peer bands to staging[q][i]), executes libtffft's
-exchange schedule with torch.distributed send/recv, runs the oracle's
-stage 3 and must land bit-exactly on the reference's forward output."""
+(self band in place, peer bands to staging[q][i][j][k]), executes libtffft's
+exchange schedule with torch.distributed send/recv into the landing buffer,
+reads the landing bands through the STRIDED_INPLACE addressing the way the GPU
+stage-3 kernel does, runs the oracle's stage 3 and must land bit-exactly on
+the reference's forward output."""
 
 import os
 import socket
@@ -36,17 +38,25 @@ def _worker(rank, world, port, shape, q):
         n0p = n0 // world
         s1 = oracle.stage1_forward(x[rank * n0p:(rank + 1) * n0p])
         spec, staging = oracle.stage1_band_staging(s1, world, rank)
-        flat = torch.from_numpy(spec.reshape(-1).copy())
         stg = torch.from_numpy(staging.reshape(-1).copy())
+        landing = torch.zeros_like(stg)
         ops = tf.exchange_schedule(n0, n1, n2, world, rank)
         reqs = []
         for op in ops:  # libtffft posts all sends and receives of a rank in one group
             reqs.append(dist.isend(stg[op.send_offset:op.send_offset + op.count].clone(), op.peer))
         for op in ops:
-            reqs.append(dist.irecv(flat[op.recv_offset:op.recv_offset + op.count], op.peer))
+            reqs.append(dist.irecv(landing[op.recv_offset:op.recv_offset + op.count], op.peer))
         for r in reqs:
             r.wait()
-        out = flat.numpy().copy()
+        # the stage-3 kernel's read addressing: block s != rank of a column comes
+        # from landing[s][i][j][k], the self block from the in-place slab
+        n1p, n2c = n1 // world, n2 // 2 + 1
+        lnd = landing.numpy().reshape(world, n0p, n1p, n2c)
+        out3 = spec.reshape(n0p, world, n1p, n2c).copy()
+        for s_ in range(world):
+            if s_ != rank:
+                out3[:, s_] = lnd[s_]
+        out = out3.reshape(-1)
         oracle.stage3(out, n0, n1, n2, world, inverse=False)
         ref = oracle.forward_all(x, world)[rank]
         q.put((rank, bool(np.array_equal(out.view(np.float64), ref.view(np.float64)))))
