@@ -181,7 +181,8 @@ def test_optional_schedules_vs_oracle(shape, p, algs, dtype):
 
     def body(ep):
         fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dtype, algorithms=algs)
-        assert set(fp.algorithms) == set(algs)
+        # the optional schedules are single-rank kernels; p > 1 keeps the default ones
+        assert set(fp.algorithms) == (set(algs) if p == 1 else set())
         spec = tf.forward(fp, slabs[ep.rank])
         f = spec.data.cpu().numpy().copy()
         back = tf.inverse(fp, spec)
