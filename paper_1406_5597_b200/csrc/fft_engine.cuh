@@ -274,19 +274,6 @@ struct Stockham {
     else x.y = reinterpret_cast<const T*>(sm)[i];
   }
 
-  // padded index of `a` when a = base + m * stride and the padding is linear in
-  // m: stride a multiple of 2^PS, or base aligned to 2^PS with m * stride < 2^PS.
-  // Then pad(base + m*stride) = pad(base) + m*pstride with a compile-time pstride,
-  // so the per-element address is an immediate offset from one per-butterfly base.
-  template <int STRIDE, int COUNT>
-  __host__ __device__ static constexpr bool linear_pad() {
-    return PS >= 30 || (STRIDE % (1 << PS) == 0) || (STRIDE * COUNT <= (1 << PS));
-  }
-  template <int STRIDE>
-  __host__ __device__ static constexpr int pstride() {
-    return PS >= 30 ? STRIDE : (STRIDE % (1 << PS) == 0 ? STRIDE + (STRIDE >> PS) : STRIDE);
-  }
-
   template <int p, int COMP>
   static __device__ __forceinline__ void store(void* sm, const cx<T>* v, int tt, int b) {
     constexpr int R = 1 << pass_bits(L, p);
@@ -295,33 +282,19 @@ struct Stockham {
     for (int u = 0; u < E / R; ++u) {
       const int j = tt + TPT * u;
       const int base = (j / NS) * NS * R + (j & (NS - 1));
-      if constexpr (linear_pad<NS, R>() && (NS % (1 << (PS >= 30 ? 0 : PS)) == 0 || NS == 1)) {
-        // NS a multiple of 2^PS, or NS == 1 with R == 2^PS (base = j*R aligned)
-        const int a0 = sidx(b, base);
 #pragma unroll
-        for (int m = 0; m < R; ++m) put<COMP>(sm, a0 + m * pstride<NS>(), v[u * R + m]);
-      } else {
-#pragma unroll
-        for (int m = 0; m < R; ++m) put<COMP>(sm, sidx(b, base + m * NS), v[u * R + m]);
-      }
+      for (int m = 0; m < R; ++m) put<COMP>(sm, sidx(b, base + m * NS), v[u * R + m]);
     }
   }
 
   template <int p, int COMP>
   static __device__ __forceinline__ void load(const void* sm, cx<T>* v, int tt, int b) {
     constexpr int R = 1 << pass_bits(L, p);
-    constexpr int STR = N / R;
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       const int j = tt + TPT * u;
-      if constexpr (PS >= 30 || STR % (1 << (PS >= 30 ? 0 : PS)) == 0) {
-        const int a0 = sidx(b, j);
 #pragma unroll
-        for (int m = 0; m < R; ++m) get<COMP>(sm, a0 + m * pstride<STR>(), v[u * R + m]);
-      } else {
-#pragma unroll
-        for (int m = 0; m < R; ++m) get<COMP>(sm, sidx(b, j + m * STR), v[u * R + m]);
-      }
+      for (int m = 0; m < R; ++m) get<COMP>(sm, sidx(b, j + m * (N / R)), v[u * R + m]);
     }
   }
 

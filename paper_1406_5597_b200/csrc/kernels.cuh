@@ -176,14 +176,6 @@ col_fft_kernel(const ColParams prm) {
     return {reinterpret_cast<cx<T>*>(prm.data) + ((long long)cq * prm.grp_stride + cr), cq, cr, valid};
   };
   const unsigned bmask = (1u << prm.band_shift) - 1u;
-  // element address = column base pointer + 32-bit element offset * sizeof(cx):
-  // one IMAD.WIDE.U32 per element (an opaque base keeps the compiler from
-  // re-associating it into a 64-bit index sum + scale, 5 instructions)
-  auto at = [](const cx<T>* base, unsigned off) -> cx<T>* {
-    unsigned long long a;
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(off), "r"((unsigned)sizeof(cx<T>)), "l"(base));
-    return reinterpret_cast<cx<T>*>(a);
-  };
   auto src = [&](const Col& col, unsigned e) -> const cx<T>* {
     if constexpr (RD == 2) {
       const int band = (int)(e >> prm.band_shift);
@@ -191,7 +183,7 @@ col_fft_kernel(const ColParams prm) {
         return reinterpret_cast<const cx<T>*>(prm.staging) + ((long long)col.cq * prm.stg_grp + col.cr) +
                (long long)band * prm.stg_band + (long long)(e & bmask) * prm.stg_within;
     }
-    return at(col.p, offset(e));
+    return col.p + offset(e);
   };
   auto prefetch = [&](const Col& col) {
 #pragma unroll
@@ -249,13 +241,13 @@ col_fft_kernel(const ColParams prm) {
             const unsigned e = SH::out_elem(tt, u, m);
             const int band = (int)(e >> prm.band_shift);
             if (band != prm.self_band) stg[band * sb + (e & bmask) * sw] = v[u * SH::RL + m];
-            else *at(cur.p, offset(e)) = v[u * SH::RL + m];
+            else cur.p[offset(e)] = v[u * SH::RL + m];
           }
       } else {
 #pragma unroll
         for (int u = 0; u < E / SH::RL; ++u)
 #pragma unroll
-          for (int m = 0; m < SH::RL; ++m) *at(cur.p, offset(SH::out_elem(tt, u, m))) = v[u * SH::RL + m];
+          for (int m = 0; m < SH::RL; ++m) cur.p[offset(SH::out_elem(tt, u, m))] = v[u * SH::RL + m];
       }
     }
     cur = next;
