@@ -103,9 +103,15 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
   static constexpr size_t X_BYTES = XCHG ? (size_t)WORD * B * S : 0;
 };
 
+#ifndef TFFFT_ROW_THREADS
+#define TFFFT_ROW_THREADS 128
+#endif
+#ifndef TFFFT_ROW_MINB
+#define TFFFT_ROW_MINB 1
+#endif
 template <int L> struct RowCfg {
   static constexpr int TPT = Shape<L>::TPT;
-  static constexpr int B = 256 / TPT > 1 ? 256 / TPT : 1;
+  static constexpr int B = TFFFT_ROW_THREADS / TPT > 1 ? TFFFT_ROW_THREADS / TPT : 1;
   static constexpr int THREADS = TPT * B;
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;  // one pad slot per E elements
   static constexpr int N = Shape<L>::N;
@@ -258,7 +264,7 @@ col_fft_kernel(const ColParams prm) {
 // r2c along n2 (packed: n2 reals -> N = n2/2 complex FFT -> n2/2+1 bins)
 // ---------------------------------------------------------------------------
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+__global__ void __launch_bounds__(RowCfg<L>::THREADS, TFFFT_ROW_MINB)
 r2c_rows_kernel(const RowParams prm) {
   using RC = RowCfg<L>;
   using SH = Shape<L>;
@@ -315,7 +321,7 @@ r2c_rows_kernel(const RowParams prm) {
 __device__ __forceinline__ unsigned long long ord(double x) { return __double_as_longlong(x); }
 
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+__global__ void __launch_bounds__(RowCfg<L>::THREADS, TFFFT_ROW_MINB)
 c2r_rows_kernel(const RowParams prm) {
   using RC = RowCfg<L>;
   using SH = Shape<L>;
