@@ -64,6 +64,14 @@ struct RowParams {
 #ifndef TFFFT_PREFETCH
 #define TFFFT_PREFETCH 1
 #endif
+// narrow (stage 1b, rows kilobytes apart) column-kernel shape: columns per CTA,
+// cp.async prefetch, persistent grid
+#ifndef TFFFT_NARROW_B
+#define TFFFT_NARROW_B 8
+#endif
+#ifndef TFFFT_NARROW_PREFETCH
+#define TFFFT_NARROW_PREFETCH 1
+#endif
 #ifndef TFFFT_COLGROUPS
 #define TFFFT_COLGROUPS 1
 #endif
@@ -74,7 +82,7 @@ struct RowParams {
 template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
-  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_COLB;
+  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_NARROW_B;
   int b = 256 / TPT > want ? 256 / TPT : want;
   while (b > 1 && (TPT * b > 1024 || (size_t)b * N * (sizeof(cx<T>) + sizeof(T)) + 4096 > 227 * 1024)) b /= 2;
   return b;
@@ -99,7 +107,11 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
   // by b*QW/B words so the wavefront covers every bank exactly once
   static constexpr int S = ((RAW + QW - 1) / QW) * QW + (QW / GB > 0 ? QW / GB : 1);
   static constexpr bool XCHG = Shape<L>::P > 1;
-  static constexpr size_t P_BYTES = TFFFT_PREFETCH ? sizeof(cx<T>) * THREADS * Shape<L>::E : 0;
+  // stage 3 (WIDE): persistent CTAs prefetch the next tile; stage 1b: one tile
+  // per CTA, several CTAs per SM overlap instead
+  static constexpr bool PREFETCH = WIDE ? TFFFT_PREFETCH : TFFFT_NARROW_PREFETCH;
+  static constexpr bool PERSISTENT = PREFETCH;
+  static constexpr size_t P_BYTES = PREFETCH ? sizeof(cx<T>) * THREADS * Shape<L>::E : 0;
   static constexpr size_t X_BYTES = XCHG ? (size_t)WORD * B * S : 0;
 };
 
@@ -200,7 +212,7 @@ col_fft_kernel(const ColParams prm) {
   long long tile = blockIdx.x;
   if (tile >= ntiles) return;
   Col cur = column(tile);
-  if (TFFFT_PREFETCH) prefetch(cur);
+  if (CF::PREFETCH) prefetch(cur);
   // tiles sharing one pf_bytes-wide row segment; each prefetches N/GT rows
   const int GT = prm.pf_ahead > 0 ? prm.pf_bytes / (B * (int)sizeof(cx<T>)) : 1;
   for (; tile < ntiles; tile += gridDim.x) {
@@ -219,7 +231,7 @@ col_fft_kernel(const ColParams prm) {
     cx<T> v[E];
     Col next = cur;
     const long long nxt = tile + gridDim.x;
-    if (TFFFT_PREFETCH) {
+    if constexpr (CF::PREFETCH) {
       cp_wait_all();
 #pragma unroll
       for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = pf[kk * NT + t];

@@ -39,11 +39,7 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   }();
   const long long tiles = (p.ncols + CF::B - 1) / CF::B;
   if (tiles <= 0) return cudaSuccess;
-#ifdef TFFFT_NONPERSISTENT
-  const long long blocks = tiles;
-#else
-  const long long blocks = std::min<long long>(tiles, (long long)per_sm * num_sms());
-#endif
+  const long long blocks = CF::PERSISTENT ? std::min<long long>(tiles, (long long)per_sm * num_sms()) : tiles;
   (void)cudaGetLastError();  // clear any stale error of this thread
   k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
   return cudaGetLastError();
