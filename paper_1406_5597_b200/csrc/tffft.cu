@@ -212,6 +212,8 @@ struct tffft_plan_s {
   void* fs_twA = nullptr;
   void* fs_twB = nullptr;
   void* fs_twN = nullptr;
+  // exchange strategy (exchange.py:48-50): 0 STRIDED (transpose-free), 1 TRANSPOSE
+  int strategy = 0;
   // fused stage 1 (stage1_fused.cuh)
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
@@ -315,6 +317,33 @@ __global__ void pull_chunks_kernel(void* const* __restrict__ ptrs, long long wor
     dst[w] = src[w];
 }
 
+// TRANSPOSE strategy pack / unpack (exchange.py:145-192): a permutation of whole
+// k-rows (n2c contiguous complex values).  Row (a, b, c) of an A x B x C
+// iteration moves from src + a*sa + b*sb + c*sc to dst + a*da + b*db + c*dc
+// (element units); with `self` >= 0, block a == self is read from src_self
+// instead (the rank's own block never crosses the exchange).  One warp per row.
+struct PermuteParams {
+  const void* src;
+  const void* src_self;
+  void* dst;
+  int A, B, C, self;
+  long long sa, sb, sc, da, db, dc;
+  long long row_words;  // words of W per row
+};
+
+template <typename W>
+__global__ void permute_rows_kernel(const PermuteParams p, int esz) {
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const long long total = (long long)p.A * p.B * p.C;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < total; r += warps) {
+    const int c = (int)(r % p.C), b = (int)((r / p.C) % p.B), a = (int)(r / ((long long)p.C * p.B));
+    const char* sbase = static_cast<const char*>(a == p.self ? p.src_self : p.src);
+    const W* s = reinterpret_cast<const W*>(sbase + (a * p.sa + b * p.sb + c * p.sc) * esz);
+    W* d = reinterpret_cast<W*>(static_cast<char*>(p.dst) + (a * p.da + b * p.db + c * p.dc) * esz);
+    for (long long w = threadIdx.x % 32; w < p.row_words; w += 32) d[w] = s[w];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // stage launchers
 // ---------------------------------------------------------------------------
@@ -333,7 +362,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   c.self_band = pl->rank;
   c.staging = nullptr;
   int rd = 0;
-  if (pl->p > 1) {
+  if (pl->p > 1 && pl->strategy == 0) {
     // forward epilogue: band q != rank -> staging[q][i][j][k];
     // inverse: band q != rank is read from landing[q][i][j][k] (the exchange output)
     c.staging = inv ? pl->landing : pl->staging;
@@ -623,6 +652,101 @@ static int fabric_pull_list(tffft_plan_t pl) {
 }
 
 // ---------------------------------------------------------------------------
+// TRANSPOSE strategy (exchange.py:195-260): local transpose into per-peer
+// blocks, contiguous exchange, rearrangement into CONTIGUOUS_FLIPPED
+// (element (j, r, k) at j*n0*n2c + r*n2c + k, layout.py:42-44)
+// ---------------------------------------------------------------------------
+static int permute(tffft_plan_t pl, const PermuteParams& prm, cudaStream_t s) {
+  const long long rows = (long long)prm.A * prm.B * prm.C;
+  const unsigned blocks = (unsigned)std::min<long long>((rows + 7) / 8, 148LL * 64);
+  pl->launches++;
+  if (pl->esz == 16)
+    permute_rows_kernel<int4><<<blocks, 256, 0, s>>>(prm, 16);
+  else
+    permute_rows_kernel<int2><<<blocks, 256, 0, s>>>(prm, 8);
+  CUDA_TRY(cudaGetLastError());
+  return TFFFT_OK;
+}
+
+static uint64_t offrank_block_bytes(tffft_plan_t pl) {
+  return (uint64_t)(pl->p - 1) * pl->n0p * pl->n1p * pl->n2c * pl->esz;
+}
+
+// forward: (n0p, n1, n2c) stage-1 output in `spec` -> staging[q][j][i][k]
+static int pack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
+  PermuteParams p{};
+  p.src = spec; p.src_self = spec; p.dst = pl->staging; p.self = -1;
+  p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
+  p.sa = n1p * n2c; p.sb = n2c; p.sc = (long long)pl->n1 * n2c;
+  p.da = band; p.db = n0p * n2c; p.dc = n2c;
+  p.row_words = n2c;
+  TRY(permute(pl, p, s));
+  pl->counters[0] += offrank_block_bytes(pl);
+  return TFFFT_OK;
+}
+// forward: blocks [src][j][i][k] (own block from staging) -> flipped (j, src*n0p + i, k) in `spec`
+static int unpack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
+  PermuteParams p{};
+  p.src = pl->p > 1 ? pl->landing : pl->staging;
+  p.dst = spec; p.self = pl->rank;
+  p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
+  p.sa = band; p.sb = n0p * n2c; p.sc = n2c;
+  p.da = n0p * n2c; p.db = (long long)pl->n0 * n2c; p.dc = n2c;
+  p.row_words = n2c;
+  p.src_self = pl->staging;  // indexed like the landing buffer: block `rank` of staging
+  TRY(permute(pl, p, s));
+  pl->counters[2] += offrank_block_bytes(pl);
+  return TFFFT_OK;
+}
+// inverse: flipped (j, dest*n0p + i, k) in `spec` -> staging[dest][j][i][k]
+static int pack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
+  PermuteParams p{};
+  p.src = spec; p.src_self = spec; p.dst = pl->staging; p.self = -1;
+  p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
+  p.sa = n0p * n2c; p.sb = (long long)pl->n0 * n2c; p.sc = n2c;
+  p.da = band; p.db = n0p * n2c; p.dc = n2c;
+  p.row_words = n2c;
+  TRY(permute(pl, p, s));
+  pl->counters[0] += offrank_block_bytes(pl);
+  return TFFFT_OK;
+}
+// inverse: blocks [src][j][i][k] -> (i, src*n1p + j, k) of the (n0p, n1, n2c) buffer `spec`
+static int unpack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
+  const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
+  PermuteParams p{};
+  p.src = pl->p > 1 ? pl->landing : pl->staging;
+  p.src_self = pl->staging;
+  p.dst = spec; p.self = pl->rank;
+  p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
+  p.sa = band; p.sb = n0p * n2c; p.sc = n2c;
+  p.da = n1p * n2c; p.db = n2c; p.dc = (long long)pl->n1 * n2c;
+  p.row_words = n2c;
+  TRY(permute(pl, p, s));
+  pl->counters[2] += offrank_block_bytes(pl);
+  return TFFFT_OK;
+}
+
+// stage 3 / 3' over the CONTIGUOUS_FLIPPED layout: column (j, k) at stride n2c
+static int stage3_flipped(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  ColParams c{};
+  c.data = spec;
+  c.tw = pl->tw0;
+  c.ncols = (long long)pl->n1p * pl->n2c;
+  c.cpb = pl->n2c;
+  c.grp_stride = (long long)pl->n0 * pl->n2c;
+  c.ic_shift = 30;
+  c.inner_stride = pl->n2c;
+  c.block_stride = 0;
+  c.band_shift = 30;
+  c.self_band = 0;
+  CUDA_TRY(col_launch(pl, pl->L0, inv, false, 0, false, c, s));
+  return TFFFT_OK;
+}
+
+// ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -726,7 +850,8 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
 
 int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   if (!pl || !flags) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
-  *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0);
+  *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0) |
+           (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0);
   return TFFFT_OK;
 }
 
@@ -746,6 +871,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   if (n0 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n0 (%d does not divide %d)", p, n0);
   if (n1 % p) return fail(TFFFT_ERR_CONFIGURATION, "p does not divide n1 (%d does not divide %d)", p, n1);
   if (dtype != TFFFT_F64 && dtype != TFFFT_F32) return fail(TFFFT_ERR_CONFIGURATION, "unknown dtype %d", dtype);
+  const int strategy = (flags & TFFFT_FLAG_TRANSPOSE) ? 1 : 0;
   // kernels address the local spectral slab with 32-bit element offsets
   if ((long long)(n0 / p) * n1 * (n2 / 2 + 1) >= (1LL << 32))
     return fail(TFFFT_ERR_SIZE, "local slab of %lld complex elements exceeds 2^32; use more ranks",
@@ -760,6 +886,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   pl->L0 = ilog2(n0); pl->L1 = ilog2(n1); pl->L2h = ilog2(n2) - 1;
   pl->n0p = n0 / p; pl->n1p = n1 / p; pl->n2c = n2 / 2 + 1;
   pl->esz = dtype == TFFFT_F64 ? 16 : 8;
+  pl->strategy = strategy;
   CUDA_TRY(cudaSetDevice(comm->device));
 
   size_t ws = 0;
@@ -770,6 +897,11 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
   CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
   ws += sizeof(unsigned long long) * 3 * pl->n0p;
+  if (p == 1 && strategy == 1) {  // TRANSPOSE packs even on one rank (exchange.py:195-219)
+    const size_t sb = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
+    CUDA_TRY(cudaMalloc(&pl->staging, sb));
+    ws += sb;
+  }
   if (p > 1) {
     const size_t sb = (size_t)p * pl->n0p * pl->n1p * pl->n2c * pl->esz;
     CUDA_TRY(cudaMalloc(&pl->staging, sb));
@@ -791,7 +923,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // element than the direct 8-column kernel, which is faster today; opt-in
     // with TFFFT_FOURSTEP=1.
     // optional schedules are single-rank kernels (no staging / landing addressing)
-    const int la = ((flags & TFFFT_FLAG_FOURSTEP_STAGE3) && p == 1) ? fourstep_la(pl->L0) : 0;
+    const int la = ((flags & TFFFT_FLAG_FOURSTEP_STAGE3) && p == 1 && strategy == 0) ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
       const long long ncols = (long long)pl->n1p * pl->n2c;
@@ -814,7 +946,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // measured at 1024^3 (profiles/r01_*): the fused persistent stage 1 keeps the
     // planes in L2 but its mixed row/column tasks run at lower occupancy; the two
     // streaming kernels are faster today, so fusion is opt-in (TFFFT_FUSE=1)
-    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && p == 1 && stage1_fused_supported(pl->L2h, pl->L1)) {
+    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && p == 1 && strategy == 0 && stage1_fused_supported(pl->L2h, pl->L1)) {
       pl->s1_fused = true;
       CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
@@ -896,6 +1028,16 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
     TRY(stage1_columns(pl, spec_out, false, s));
   }
   MARK(ev, 1, s);
+  if (pl->strategy == 1) {
+    // TRANSPOSE (exchange.py:195-219): pack -> contiguous exchange -> unpack
+    TRY(pack_forward(pl, spec_out, s));
+    TRY(exchange(pl, spec_out, s));
+    TRY(unpack_forward(pl, spec_out, s));
+    MARK(ev, 2, s);
+    TRY(stage3_flipped(pl, spec_out, false, s));
+    MARK(ev, 3, s);
+    return TFFFT_OK;
+  }
   // exchange (exchange.py:263-276)
   TRY(exchange(pl, spec_out, s));
   MARK(ev, 2, s);
@@ -916,11 +1058,21 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   CUDA_TRY(cudaMemsetAsync(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p, s));
   // stage 3' (dfft.py:196-197)
   TRY(fabric_guard_staging(pl, s));
-  TRY(stage3_columns(pl, spec, true, s));
-  MARK(ev, 1, s);
-  // exchange (exchange.py:279-290)
-  TRY(exchange(pl, spec, s));
-  MARK(ev, 2, s);
+  if (pl->strategy == 1) {
+    TRY(stage3_flipped(pl, spec, true, s));
+    MARK(ev, 1, s);
+    // TRANSPOSE (exchange.py:222-260): pack -> contiguous exchange -> un-transpose
+    TRY(pack_inverse(pl, spec, s));
+    TRY(exchange(pl, spec, s));
+    TRY(unpack_inverse(pl, spec, s));
+    MARK(ev, 2, s);
+  } else {
+    TRY(stage3_columns(pl, spec, true, s));
+    MARK(ev, 1, s);
+    // exchange (exchange.py:279-290)
+    TRY(exchange(pl, spec, s));
+    MARK(ev, 2, s);
+  }
   // stage 1' (dfft.py:206-209)
   if (pl->s1_fused) {
     TRY(stage1_fused(pl, real_out, spec, false, s));

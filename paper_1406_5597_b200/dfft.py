@@ -116,6 +116,11 @@ class FftPlan:
 
 
 ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2}
+TRANSPOSE_FLAG = 4
+
+
+def _spectral_tag(strategy: Strategy) -> SpectralTag:
+    return SpectralTag.STRIDED_INPLACE if strategy is Strategy.STRIDED else SpectralTag.CONTIGUOUS_FLIPPED
 
 
 def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED,
@@ -127,8 +132,6 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     "fourstep_stage3"); None takes the library defaults (TFFFT_FUSE /
     TFFFT_FOURSTEP environment switches)."""
     validate(grid, comm.p)
-    if strategy is not Strategy.STRIDED:
-        raise ConfigurationError("the B200 path implements the transpose-free STRIDED strategy only")
     if comm_pattern is not CommPattern.PAIRWISE:
         raise ConfigurationError("the B200 path implements the PAIRWISE comm pattern only")
     if dtype not in DTYPES:
@@ -140,6 +143,8 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
         if unknown:
             raise ConfigurationError(f"unknown algorithms {sorted(unknown)}; choose from {sorted(ALGORITHM_FLAGS)}")
         flags = sum(ALGORITHM_FLAGS[a] for a in set(algorithms))
+    if strategy is Strategy.TRANSPOSE:  # the paper's baseline: pack, contiguous exchange, unpack
+        flags = (0 if flags < 0 else flags) | TRANSPOSE_FLAG
     h = ctypes.c_void_p()
     with torch.cuda.device(comm.device):
         _lib.check(_lib.lib().tffft_plan_create_ex(grid.n0, grid.n1, grid.n2, code, 0, flags, comm.handle,
@@ -174,8 +179,10 @@ def forward(fp: FftPlan, real: RealSlab, out: torch.Tensor | None = None) -> Spe
     """Distributed forward r2c of this rank's slab (dfft.py:148-176).
 
     Collective.  Logical element (j, r, k) of the result is bin
-    (r, rank*(n1/p)+j, k) of the unnormalised global spectrum.  The result is
-    backed by plan memory unless ``out`` is given."""
+    (r, rank*(n1/p)+j, k) of the unnormalised global spectrum, stored
+    STRIDED_INPLACE (Strategy.STRIDED) or CONTIGUOUS_FLIPPED
+    (Strategy.TRANSPOSE).  The result is backed by plan memory unless ``out``
+    is given."""
     if real.layout != fp.real_layout:
         raise ContractError(f"slab layout {real.layout} does not match plan {fp.real_layout}")
     _, rdt, cdt = DTYPES[fp.dtype]
@@ -186,7 +193,7 @@ def forward(fp: FftPlan, real: RealSlab, out: torch.Tensor | None = None) -> Spe
         raise ContractError(f"spectral output needs {fp.work1.numel()} elements, got {dst.numel()}")
     _lib.check(_lib.lib().tffft_forward(fp.handle, ctypes.c_void_p(real.data.data_ptr()),
                                         ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
-    return SpectralSlab(fp.spectral_layout, SpectralTag.STRIDED_INPLACE, dst)
+    return SpectralSlab(fp.spectral_layout, _spectral_tag(fp.strategy), dst)
 
 
 def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) -> RealSlab:
@@ -195,8 +202,9 @@ def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) ->
     Collective; consumes ``spec`` in place.  With ``fp.check_consistency`` the
     call synchronises and raises ConsistencyError for a non-Hermitian half
     spectrum, as the reference's _c2r_rows does (kernels.py:223-238)."""
-    if spec.tag is not SpectralTag.STRIDED_INPLACE:
-        raise ContractError(f"plan strategy {fp.strategy} expects a {SpectralTag.STRIDED_INPLACE} slab, got {spec.tag}")
+    expected = _spectral_tag(fp.strategy)
+    if spec.tag is not expected:
+        raise ContractError(f"plan strategy {fp.strategy} expects a {expected} slab, got {spec.tag}")
     if spec.layout != fp.spectral_layout:
         raise ContractError(f"slab layout {spec.layout} does not match plan")
     _, rdt, cdt = DTYPES[fp.dtype]

@@ -266,3 +266,42 @@ def test_host_pair_stream_matches_device_path():
     tf.HostPairStream(fp).run(h_in, h_out)
     for x, h in zip(xs, h_out):
         assert rel(h.numpy().reshape(shape), x) <= 1e-12
+
+
+@pytest.mark.parametrize("shape,p", [((8, 8, 8), 1), ((16, 16, 16), 2), ((32, 16, 8), 4), ((16, 8, 32), 8),
+                                     ((128, 128, 128), 2), ((64, 64, 64), 1)], ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_transpose_strategy_equivalence(shape, p, dtype):
+    """Strategy.TRANSPOSE (pack -> exchange -> unpack, CONTIGUOUS_FLIPPED) gives
+    the same logical spectrum as STRIDED bit for bit (cli.py:192-198 'strategy
+    equivalence'), round-trips, and counts the reference's copy bytes:
+    packed = wire = unpacked = off-rank bytes, vs STRIDED's (0, wire, 0)."""
+    x = oracle.uniform_field(shape, seed=13 + p)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        out = {}
+        for strat in (tf.Strategy.STRIDED, tf.Strategy.TRANSPOSE):
+            fp = tf.plan(grid, ep, strat, dtype=dtype)
+            fp.reset_instrumentation()
+            spec = tf.forward(fp, slabs[ep.rank])
+            logical = spec.as_logical().cpu().numpy().copy()
+            back = tf.inverse(fp, spec)
+            out[strat] = (logical, back.data.cpu().numpy().copy(), fp.counters.snapshot(), spec.tag)
+            fp.close()
+        return out
+
+    res = tf.run_spmd(p, body)
+    n0p, n1p, n2c = shape[0] // p, shape[1] // p, shape[2] // 2 + 1
+    esz = 16 if dtype == "float64" else 8
+    off = (p - 1) * n0p * n1p * n2c * esz
+    for q in range(p):
+        s, t = res[q][tf.Strategy.STRIDED], res[q][tf.Strategy.TRANSPOSE]
+        assert t[3] is tf.SpectralTag.CONTIGUOUS_FLIPPED and s[3] is tf.SpectralTag.STRIDED_INPLACE
+        assert np.array_equal(s[0], t[0])                    # bitwise strategy equivalence
+        assert rel(t[1].reshape(-1), x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
+        assert s[2] == (0, 2 * off, 0)
+        assert t[2] == (2 * off, 2 * off, 2 * off)
