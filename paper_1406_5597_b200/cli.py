@@ -6,8 +6,9 @@
            triple sum evaluated with torch on the device (oracle.py:30-45)
   bench    forward+inverse pairs, per-stage times and copy counters as CSV
            with the reference's header (cli.py:32-47, 319-339)
-  compare  the reference A/B against the TRANSPOSE strategy; that strategy is
-           not part of the B200 path, so it exits with a configuration error
+  compare  the paper's A/B: STRIDED (transpose-free) against TRANSPOSE on
+           identical inputs, median times, copy-byte ratio and a bitwise
+           strategy-equivalence check (cli.py:342-383)
 
 Exit codes (cli.py:440-456): 0 all checks passed, 1 a check failed,
 2 usage or configuration error.  Ranks are host threads over the in-process
@@ -89,14 +90,21 @@ def _verify_grids(max_size: int) -> list[GlobalGrid]:
     return grids
 
 
-def _run_pipeline(grid: GlobalGrid, p: int, field: torch.Tensor, iters: int = 0, warmup: int = 0):
+def _parse_strategies(text: str) -> list[Strategy]:
+    if text == "both":
+        return [Strategy.STRIDED, Strategy.TRANSPOSE]
+    return [Strategy(text)]
+
+
+def _run_pipeline(grid: GlobalGrid, p: int, field: torch.Tensor, iters: int = 0, warmup: int = 0,
+                  strategy: Strategy = Strategy.STRIDED):
     """forward (+ inverse pairs when timing) on p ranks; returns the gathered
     spectrum, per-iteration records (wall us, stage dict, counters) merged
     over ranks, and the worst round-trip relative rms (cli.py:87-128)."""
     slabs = scatter_real(field, grid, p)
 
     def body(ep):
-        fp = plan(grid, ep, Strategy.STRIDED, check_consistency=True)
+        fp = plan(grid, ep, strategy, check_consistency=True)
         fp.enable_timing(True)
         mine = slabs[ep.rank]
         recs = []
@@ -128,6 +136,15 @@ def _run_pipeline(grid: GlobalGrid, p: int, field: torch.Tensor, iters: int = 0,
     return gathered, merged, max(r[2] for r in per_rank)
 
 
+def _check(report, failures, grid, p, strategy, name, err, tol):
+    status = "PASS" if err <= tol else "FAIL"
+    line = (f"{grid.n0}x{grid.n1}x{grid.n2} p={p} {strategy:9s} {name:22s} "
+            f"max_error={err:.3e} (tol {tol:.1e}) {status}")
+    report.append(line)
+    if status == "FAIL":
+        failures.append(line)
+
+
 def cmd_verify(args) -> int:
     if args.max_size > MAX_VERIFY_SIZE:
         print(f"usage error: --max-size is capped at {MAX_VERIFY_SIZE} (brute-force oracle cost)")
@@ -143,15 +160,19 @@ def cmd_verify(args) -> int:
                 validate(grid, p)
             except ConfigurationError:
                 continue
-            gathered, _, rel = _run_pipeline(grid, p, field)
-            for name, err, tol in (("oracle_equivalence", float(abs(gathered - ref).max()), ORACLE_ATOL),
-                                   ("round_trip", rel, ROUNDTRIP_RTOL)):
-                status = "PASS" if err <= tol else "FAIL"
-                line = (f"{grid.n0}x{grid.n1}x{grid.n2} p={p} strided   {name:22s} "
-                        f"max_error={err:.3e} (tol {tol:.1e}) {status}")
-                report.append(line)
-                if status == "FAIL":
-                    failures.append(line)
+            spectra = {}
+            for strategy in args.strategies:
+                gathered, _, rel = _run_pipeline(grid, p, field, strategy=strategy)
+                spectra[strategy] = gathered
+                for name, err, tol in (("oracle_equivalence", float(abs(gathered - ref).max()), ORACLE_ATOL),
+                                       ("round_trip", rel, ROUNDTRIP_RTOL)):
+                    _check(report, failures, grid, p, strategy.value, name, err, tol)
+                    checks += 1
+            if len(spectra) == 2:
+                a = spectra[Strategy.STRIDED].view("float64")
+                b = spectra[Strategy.TRANSPOSE].view("float64")
+                diff = 0.0 if (a == b).all() else float(abs(a - b).max())
+                _check(report, failures, grid, p, "both", "strategy_equivalence", diff, 0.0)
                 checks += 1
     for line in report:
         print(line)
@@ -166,21 +187,23 @@ def cmd_bench(args) -> int:
     grid = args.size
     rows = []
     for p in args.procs:
+      for strategy in args.strategies:
         validate(grid, p)
         field = _random_field(grid, args.seed)
-        _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup)
+        _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
         if rel > ROUNDTRIP_RTOL:
             raise SlabFftError(f"embedded correctness cross-check failed: round-trip error {rel:.3e} "
                                f"exceeds {ROUNDTRIP_RTOL:.1e} on {grid.n0}x{grid.n1}x{grid.n2}, p={p}")
         for it, (wall, st, cnt) in enumerate(merged):
             rows.append({"grid_n0": grid.n0, "grid_n1": grid.n1, "grid_n2": grid.n2, "p": p,
-                         "strategy": "strided", "comm_pattern": "pairwise", "iter": it,
+                         "strategy": strategy.value, "comm_pattern": "pairwise", "iter": it,
                          "t_total_us": f"{wall:.3f}", "t_stage1_us": f"{st['stage1_us']:.3f}",
                          "t_exchange_us": f"{st['exchange_us']:.3f}", "t_stage3_us": f"{st['stage3_us']:.3f}",
                          "bytes_packed": cnt[0], "bytes_wire": cnt[1], "bytes_unpacked": cnt[2]})
-        med = statistics.median(float(r["t_total_us"]) for r in rows if r["p"] == p)
-        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  comm=pairwise  mode=threaded  iters={args.iters}  "
-              f"median pair {med:.1f} us", file=sys.stderr)
+        med = statistics.median(float(r["t_total_us"]) for r in rows
+                                if r["p"] == p and r["strategy"] == strategy.value)
+        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  {strategy.value}  comm=pairwise  mode=threaded  "
+              f"iters={args.iters}  median pair {med:.1f} us", file=sys.stderr)
     out = open(args.output, "w", newline="") if args.output else sys.stdout
     writer = csv.DictWriter(out, fieldnames=CSV_COLUMNS)
     writer.writeheader()
@@ -191,9 +214,43 @@ def cmd_bench(args) -> int:
 
 
 def cmd_compare(args) -> int:
-    print("configuration error: the B200 path implements the transpose-free STRIDED strategy only; "
-          "the TRANSPOSE baseline of the A/B comparison is out of scope")
-    return 2
+    """Both strategies on identical inputs (cli.py:342-383)."""
+    if args.iters < 1:
+        print("usage error: --iters must be >= 1")
+        return 2
+    grid = args.size
+    field = _random_field(grid, args.seed)
+    status = 0
+    for p in args.procs:
+        validate(grid, p)
+        res = {}
+        for strategy in (Strategy.STRIDED, Strategy.TRANSPOSE):
+            gathered, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
+            if rel > ROUNDTRIP_RTOL:
+                raise SlabFftError(f"round-trip error {rel:.3e} exceeds {ROUNDTRIP_RTOL:.1e} for {strategy.value}")
+            res[strategy] = (gathered, merged)
+        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  comm=pairwise  mode=threaded  iters={args.iters}")
+        print(f"{'strategy':10s} {'t_total_us(med)':>16s} {'t_exchange_us(med)':>19s} "
+              f"{'packed':>12s} {'wire':>12s} {'unpacked':>12s}")
+        totals = {}
+        for strategy, (_, merged) in res.items():
+            tot = statistics.median(m[0] for m in merged)
+            exch = statistics.median(m[1]["exchange_us"] for m in merged)
+            cnt = merged[-1][2]
+            totals[strategy] = (tot, sum(cnt))
+            print(f"{strategy.value:10s} {tot:16.1f} {exch:19.1f} {cnt[0]:12d} {cnt[1]:12d} {cnt[2]:12d}")
+        s_bytes, t_bytes = totals[Strategy.STRIDED][1], totals[Strategy.TRANSPOSE][1]
+        if s_bytes > 0:
+            print(f"copy-byte ratio transpose/strided: {t_bytes / s_bytes:.2f}")
+        else:
+            print("copy-byte ratio transpose/strided: n/a (no exchanged bytes at p=1)")
+        t_t, t_s = totals[Strategy.TRANSPOSE][0], totals[Strategy.STRIDED][0]
+        print(f"median pair time: strided {100.0 * (t_t - t_s) / t_t:+.1f}% vs transpose (B200, device-timed)")
+        same = (res[Strategy.STRIDED][0].view("float64") == res[Strategy.TRANSPOSE][0].view("float64")).all()
+        print(f"spectra bitwise identical: {'yes' if same else 'NO'}")
+        if not same:
+            status = 1
+    return status
 
 
 def build_parser() -> argparse.ArgumentParser:
@@ -203,6 +260,8 @@ def build_parser() -> argparse.ArgumentParser:
     pv = sub.add_parser("verify", help="oracle-equivalence and round-trip suites")
     pv.add_argument("--max-size", type=int, default=8)
     pv.add_argument("--procs", type=_parse_procs, default=[1, 2, 4])
+    pv.add_argument("--strategy", dest="strategies", type=_parse_strategies,
+                    default=[Strategy.STRIDED, Strategy.TRANSPOSE])
     pv.add_argument("--seed", type=int, default=0)
     pv.set_defaults(func=cmd_verify)
     pb = sub.add_parser("bench", help="time forward+inverse pairs and emit CSV")
@@ -211,11 +270,15 @@ def build_parser() -> argparse.ArgumentParser:
     pb.add_argument("--iters", type=int, default=5)
     pb.add_argument("--warmup", type=int, default=1)
     pb.add_argument("--output", default=None)
+    pb.add_argument("--strategy", dest="strategies", type=_parse_strategies, default=[Strategy.STRIDED])
     pb.add_argument("--seed", type=int, default=0)
     pb.set_defaults(func=cmd_bench)
-    pc = sub.add_parser("compare", help="strategy A/B (TRANSPOSE is out of scope on B200)")
+    pc = sub.add_parser("compare", help="run both strategies on identical inputs")
     pc.add_argument("--size", type=_parse_size, required=True)
     pc.add_argument("--procs", type=_parse_procs, default=[4])
+    pc.add_argument("--iters", type=int, default=5)
+    pc.add_argument("--warmup", type=int, default=1)
+    pc.add_argument("--seed", type=int, default=0)
     pc.set_defaults(func=cmd_compare)
     return parser
 

@@ -13,7 +13,7 @@ def test_usage_errors_exit_2():
     assert cli.main(["verify", "--max-size", "64"]) == 2          # cli.py:160-162
     assert cli.main(["verify", "--max-size", "8", "--procs", "3"]) == 2  # p does not divide
     assert cli.main(["bench", "--size", "8", "--iters", "0"]) == 2
-    assert cli.main(["compare", "--size", "8"]) == 2               # TRANSPOSE out of scope
+    assert cli.main(["compare", "--size", "8", "--iters", "0"]) == 2
     assert cli.main(["nonsense"]) == 2
 
 
@@ -42,3 +42,11 @@ def test_bench_csv(tmp_path):
         p = int(r["p"])
         # wire bytes per pair, summed over ranks: 2 * p * (p-1) * n0p * n1p * n2c * 16
         assert int(r["bytes_wire"]) == 2 * p * (p - 1) * (16 // p) * (16 // p) * 9 * 16
+
+
+@pytest.mark.gpu
+def test_compare_strategies(capsys):
+    assert cli.main(["compare", "--size", "32", "--procs", "2,4", "--iters", "2"]) == 0
+    out = capsys.readouterr().out
+    assert out.count("spectra bitwise identical: yes") == 2
+    assert out.count("copy-byte ratio transpose/strided: 3.00") == 2
