@@ -180,6 +180,25 @@ def cmd_verify(args) -> int:
     return 0 if not failures else 1
 
 
+def _bench_rows(grid: GlobalGrid, p: int, strategy: Strategy, args) -> list[dict]:
+    field = _random_field(grid, args.seed)
+    _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
+    if rel > ROUNDTRIP_RTOL:
+        raise SlabFftError(f"embedded correctness cross-check failed: round-trip error {rel:.3e} "
+                           f"exceeds {ROUNDTRIP_RTOL:.1e} on {grid.n0}x{grid.n1}x{grid.n2}, p={p}")
+    rows = []
+    for it, (wall, st, cnt) in enumerate(merged):
+        rows.append({"grid_n0": grid.n0, "grid_n1": grid.n1, "grid_n2": grid.n2, "p": p,
+                     "strategy": strategy.value, "comm_pattern": "pairwise", "iter": it,
+                     "t_total_us": f"{wall:.3f}", "t_stage1_us": f"{st['stage1_us']:.3f}",
+                     "t_exchange_us": f"{st['exchange_us']:.3f}", "t_stage3_us": f"{st['stage3_us']:.3f}",
+                     "bytes_packed": cnt[0], "bytes_wire": cnt[1], "bytes_unpacked": cnt[2]})
+    med = statistics.median(float(r["t_total_us"]) for r in rows)
+    print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  {strategy.value}  comm=pairwise  mode=threaded  "
+          f"iters={args.iters}  median pair {med:.1f} us", file=sys.stderr)
+    return rows
+
+
 def cmd_bench(args) -> int:
     if args.iters < 1:
         print("usage error: --iters must be >= 1")
@@ -187,23 +206,9 @@ def cmd_bench(args) -> int:
     grid = args.size
     rows = []
     for p in args.procs:
-      for strategy in args.strategies:
         validate(grid, p)
-        field = _random_field(grid, args.seed)
-        _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
-        if rel > ROUNDTRIP_RTOL:
-            raise SlabFftError(f"embedded correctness cross-check failed: round-trip error {rel:.3e} "
-                               f"exceeds {ROUNDTRIP_RTOL:.1e} on {grid.n0}x{grid.n1}x{grid.n2}, p={p}")
-        for it, (wall, st, cnt) in enumerate(merged):
-            rows.append({"grid_n0": grid.n0, "grid_n1": grid.n1, "grid_n2": grid.n2, "p": p,
-                         "strategy": strategy.value, "comm_pattern": "pairwise", "iter": it,
-                         "t_total_us": f"{wall:.3f}", "t_stage1_us": f"{st['stage1_us']:.3f}",
-                         "t_exchange_us": f"{st['exchange_us']:.3f}", "t_stage3_us": f"{st['stage3_us']:.3f}",
-                         "bytes_packed": cnt[0], "bytes_wire": cnt[1], "bytes_unpacked": cnt[2]})
-        med = statistics.median(float(r["t_total_us"]) for r in rows
-                                if r["p"] == p and r["strategy"] == strategy.value)
-        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  {strategy.value}  comm=pairwise  mode=threaded  "
-              f"iters={args.iters}  median pair {med:.1f} us", file=sys.stderr)
+        for strategy in args.strategies:
+            rows += _bench_rows(grid, p, strategy, args)
     out = open(args.output, "w", newline="") if args.output else sys.stdout
     writer = csv.DictWriter(out, fieldnames=CSV_COLUMNS)
     writer.writeheader()
