@@ -79,9 +79,12 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
 enum {
   TFFFT_FLAG_FUSED_STAGE1 = 1,   /* one persistent kernel per direction for stage 1 (planes in L2) */
   TFFFT_FLAG_FOURSTEP_STAGE3 = 2, /* stage 3 as an L2-resident four-step with 1 KB row visits */
-  TFFFT_FLAG_TRANSPOSE = 4        /* Strategy.TRANSPOSE (exchange.py:195-260): pack, contiguous exchange,
+  TFFFT_FLAG_TRANSPOSE = 4,       /* Strategy.TRANSPOSE (exchange.py:195-260): pack, contiguous exchange,
                                      unpack; the spectrum comes out CONTIGUOUS_FLIPPED, element (j, r, k)
                                      at j*n0*n2c + r*n2c + k (layout.py:42-44) -- the paper's baseline */
+  TFFFT_FLAG_PEER_STORES = 8      /* fused exchange: the stage-1 / stage-3' epilogues store every peer band
+                                     straight into the peer's landing buffer (peer memory), and the
+                                     exchange reduces to a barrier.  Local fabric communicators. */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

@@ -21,7 +21,9 @@ namespace tffft {
 //   -> staging + band*stg_band + (e & band_mask)*stg_within + (c / cpb)*stg_grp + (c % cpb)
 struct ColParams {
   void* data;
-  void* staging;          // RD == 1: peer bands written here; RD == 2: peer bands read from here (landing)
+  void* staging;          // RD == 2: peer bands read from here (landing)
+  void* const* band_dst;  // RD == 1: destination block of band q (p pointers): the rank's
+                          // staging block q, or -- peer stores -- rank q's landing block for us
   const void* tw;
   long long ncols;
   int cpb;
@@ -250,16 +252,21 @@ col_fft_kernel(const ColParams prm) {
 
     if (cur.valid) {
       if constexpr (RD == 1) {
-        cx<T>* stg = reinterpret_cast<cx<T>*>(prm.staging) + ((long long)cur.cq * prm.stg_grp + cur.cr);
-        const unsigned sb = (unsigned)prm.stg_band, sw = (unsigned)prm.stg_within;
+        const long long cofs = (long long)cur.cq * prm.stg_grp + cur.cr;
+        const unsigned sw = (unsigned)prm.stg_within;
 #pragma unroll
         for (int u = 0; u < E / SH::RL; ++u)
 #pragma unroll
           for (int m = 0; m < SH::RL; ++m) {
             const unsigned e = SH::out_elem(tt, u, m);
             const int band = (int)(e >> prm.band_shift);
-            if (band != prm.self_band) stg[band * sb + (e & bmask) * sw] = v[u * SH::RL + m];
-            else cur.p[offset(e)] = v[u * SH::RL + m];
+            if (band != prm.self_band) {
+              cx<T>* dst = reinterpret_cast<cx<T>*>(
+                  __ldg(reinterpret_cast<const unsigned long long*>(prm.band_dst) + band));
+              dst[cofs + (long long)(e & bmask) * sw] = v[u * SH::RL + m];
+            } else {
+              cur.p[offset(e)] = v[u * SH::RL + m];
+            }
           }
       } else {
 #pragma unroll

@@ -127,7 +127,7 @@ struct LocalFabric {
   double timeout_s = 600.0;
   // per plan sequence number: each rank's staging pointer and events
   struct Slot {
-    std::vector<void*> staging;
+    std::vector<void*> staging, landing;
     std::vector<cudaEvent_t> ready, done;
   };
   std::vector<Slot> slots;
@@ -167,6 +167,7 @@ struct LocalFabric {
     Slot& s = slots[seq];
     if ((int)s.staging.size() != p) {
       s.staging.assign(p, nullptr);
+      s.landing.assign(p, nullptr);
       s.ready.assign(p, nullptr);
       s.done.assign(p, nullptr);
     }
@@ -199,6 +200,8 @@ struct tffft_plan_s {
   int seq = 0;
   void* staging = nullptr;   // outgoing peer bands [q][i][j][k]
   void* landing = nullptr;   // incoming peer bands [q][i][j][k]
+  void** band_dst = nullptr; // device: destination block of each outgoing band (p pointers)
+  bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
   void* tw0 = nullptr;
   void* tw1 = nullptr;
   void* tw2 = nullptr;
@@ -363,9 +366,10 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   c.staging = nullptr;
   int rd = 0;
   if (pl->p > 1 && pl->strategy == 0) {
-    // forward epilogue: band q != rank -> staging[q][i][j][k];
+    // forward epilogue: band q != rank -> band_dst[q] (staging[q], or rank q's landing[rank]);
     // inverse: band q != rank is read from landing[q][i][j][k] (the exchange output)
-    c.staging = inv ? pl->landing : pl->staging;
+    c.staging = pl->landing;
+    c.band_dst = pl->band_dst;
     rd = inv ? 2 : 1;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = pl->n2c;
@@ -508,8 +512,9 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   int rd = 0;
   if (pl->p > 1) {
     // forward: block s != rank is read from landing[s][i][c] (the exchange output);
-    // inverse epilogue: block s != rank -> staging[s][i][c]
-    c.staging = inv ? pl->staging : pl->landing;
+    // inverse epilogue: block s != rank -> band_dst[s] (staging[s], or rank s's landing[rank])
+    c.staging = pl->landing;
+    c.band_dst = pl->band_dst;
     rd = inv ? 1 : 2;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = (long long)pl->n1p * pl->n2c;
@@ -570,11 +575,40 @@ static uint64_t wire_bytes(tffft_plan_t pl) {
 }
 
 // all peers must have finished pulling from my staging before I overwrite it
+// Before this rank's epilogue writes its outgoing bands: in pull mode, every
+// peer must have finished pulling from our staging; with peer stores, every
+// peer must have finished reading its landing buffer (the host barrier makes
+// sure each peer recorded that event for the previous exchange).
 static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
   if (pl->p == 1 || pl->comm->is_nccl) return TFFFT_OK;
   auto& slot = pl->comm->fabric->slot(pl->seq);
+  if (pl->peer_stores) TRY(pl->comm->fabric->barrier());
   for (int q = 0; q < pl->p; ++q)
     if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.done[q], 0));
+  return TFFFT_OK;
+}
+
+// peer stores: this rank has consumed its landing buffer
+static int fabric_landing_consumed(tffft_plan_t pl, cudaStream_t s) {
+  if (!pl->peer_stores) return TFFFT_OK;
+  CUDA_TRY(cudaEventRecord(pl->comm->fabric->slot(pl->seq).done[pl->rank], s));
+  return TFFFT_OK;
+}
+
+// destination block of each outgoing band for the write-redirect epilogues
+static int build_band_dst(tffft_plan_t pl) {
+  const size_t band = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
+  std::vector<void*> h(pl->p, nullptr);
+  for (int q = 0; q < pl->p; ++q) {
+    if (pl->peer_stores) {
+      auto& slot = pl->comm->fabric->slot(pl->seq);
+      h[q] = static_cast<char*>(slot.landing[q]) + (size_t)pl->rank * band;  // rank q's landing block for us
+    } else {
+      h[q] = static_cast<char*>(pl->staging) + (size_t)q * band;
+    }
+  }
+  CUDA_TRY(cudaMalloc(&pl->band_dst, sizeof(void*) * pl->p));
+  CUDA_TRY(cudaMemcpy(pl->band_dst, h.data(), sizeof(void*) * pl->p, cudaMemcpyHostToDevice));
   return TFFFT_OK;
 }
 
@@ -587,6 +621,18 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
   (void)spec;
   if (pl->p == 1) return TFFFT_OK;
   const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
+  if (pl->peer_stores) {
+    // the epilogue already stored every band into its peer's landing buffer:
+    // the exchange is the barrier after which every rank's stores are visible
+    LocalFabric& fab = *pl->comm->fabric;
+    auto& slot = fab.slot(pl->seq);
+    CUDA_TRY(cudaEventRecord(slot.ready[pl->rank], s));
+    TRY(fab.barrier());
+    for (int q = 0; q < pl->p; ++q)
+      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.ready[q], 0));
+    pl->counters[1] += wire_bytes(pl);
+    return TFFFT_OK;
+  }
   if (pl->comm->is_nccl) {
     NcclApi& api = nccl();
     const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
@@ -630,6 +676,7 @@ static int fabric_setup(tffft_plan_t pl, void* /*unused*/) {
   LocalFabric& fab = *pl->comm->fabric;
   auto& slot = fab.slot(pl->seq);
   slot.staging[pl->rank] = pl->staging;
+  slot.landing[pl->rank] = pl->landing;
   CUDA_TRY(cudaEventCreateWithFlags(&slot.ready[pl->rank], cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&slot.done[pl->rank], cudaEventDisableTiming));
   TRY(fab.barrier());
@@ -851,7 +898,7 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
 int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   if (!pl || !flags) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0) |
-           (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0);
+           (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0) | (pl->peer_stores ? TFFFT_FLAG_PEER_STORES : 0);
   return TFFFT_OK;
 }
 
@@ -912,9 +959,11 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
       CUDA_TRY(cudaMalloc(&pl->pull_ptrs, nptr * sizeof(void*)));
       ws += nptr * sizeof(void*);
       pl->seq = comm->plan_seq++;
+      pl->peer_stores = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
       TRY(fabric_setup(pl.get(), nullptr));
       TRY(fabric_pull_list(pl.get()));
     }
+    TRY(build_band_dst(pl.get()));
   }
   // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
   {
@@ -982,6 +1031,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   free_events(pl);
   cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
   cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
+  cudaFree(pl->band_dst);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
@@ -1043,6 +1093,7 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
   MARK(ev, 2, s);
   // stage 3: strided columns (dfft.py:170-171)
   TRY(stage3_columns(pl, spec_out, false, s));
+  TRY(fabric_landing_consumed(pl, s));
   MARK(ev, 3, s);
   return TFFFT_OK;
 }
@@ -1078,6 +1129,7 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
     TRY(stage1_fused(pl, real_out, spec, false, s));
   } else {
     TRY(stage1_columns(pl, spec, true, s));
+    TRY(fabric_landing_consumed(pl, s));
     CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
   }
   MARK(ev, 3, s);

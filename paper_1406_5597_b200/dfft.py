@@ -115,7 +115,7 @@ class FftPlan:
             pass
 
 
-ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2}
+ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8}
 TRANSPOSE_FLAG = 4
 
 
