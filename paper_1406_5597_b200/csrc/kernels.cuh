@@ -74,6 +74,16 @@ struct RowParams {
 #ifndef TFFFT_NARROW_PREFETCH
 #define TFFFT_NARROW_PREFETCH 1
 #endif
+// Cluster pairing: a tile of CL*B columns is split over a thread-block cluster
+// of CL CTAs (B columns each).  The CTAs of a cluster run side by side, so the
+// two halves of each 128-byte line are fetched together, while every SM hosts
+// more, independently-barriered CTAs.
+#ifndef TFFFT_COLCLUSTER
+#define TFFFT_COLCLUSTER 1
+#endif
+#ifndef TFFFT_COLCLUSTER_SYNC
+#define TFFFT_COLCLUSTER_SYNC 0
+#endif
 #ifndef TFFFT_COLGROUPS
 #define TFFFT_COLGROUPS 1
 #endif
@@ -91,7 +101,9 @@ __host__ __device__ constexpr int col_batch() {
 }
 template <typename T, int L, bool WIDE = false> struct ColCfg {
   static constexpr int TPT = Shape<L>::TPT;
-  static constexpr int B = col_batch<T, L, WIDE>();
+  static constexpr int CL = (col_batch<T, L, WIDE>() % TFFFT_COLCLUSTER == 0 &&
+                             TPT * (col_batch<T, L, WIDE>() / TFFFT_COLCLUSTER) >= 128) ? TFFFT_COLCLUSTER : 1;
+  static constexpr int B = col_batch<T, L, WIDE>() / CL;     // columns per CTA
   static constexpr int THREADS = TPT * B;
   // The CTA's B columns are split over GROUPS independent thread groups (own
   // exchange buffer, own named barrier): their smem-exchange and FP64 phases
@@ -180,7 +192,9 @@ col_fft_kernel(const ColParams prm) {
   const unsigned bs = (unsigned)prm.block_stride;
   const unsigned ics = (unsigned)prm.ic_shift;
   const unsigned icm = (1u << ics) - 1u;
-  const long long ntiles = (prm.ncols + B - 1) / B;
+  constexpr int CL = CF::CL;
+  const int cl_rank = CL > 1 ? (int)(blockIdx.x % CL) : 0;   // cluster dims (CL, 1, 1)
+  const long long ntiles = (prm.ncols + CL * B - 1) / (CL * B);
 
   auto offset = [&](unsigned e) -> unsigned {
     if constexpr (TWO) return (e & icm) * is + (e >> ics) * bs;
@@ -188,7 +202,7 @@ col_fft_kernel(const ColParams prm) {
   };
   struct Col { cx<T>* p; unsigned cq, cr; bool valid; };
   auto column = [&](long long tile) -> Col {
-    const long long c_raw = tile * B + b;
+    const long long c_raw = tile * (CL * B) + cl_rank * B + b;
     const bool valid = c_raw < prm.ncols;
     const unsigned c = (unsigned)(valid ? c_raw : prm.ncols - 1);  // clamp: loads stay in bounds
     const unsigned cq = c / (unsigned)prm.cpb;
@@ -211,13 +225,17 @@ col_fft_kernel(const ColParams prm) {
     cp_commit();
   };
 
-  long long tile = blockIdx.x;
+  long long tile = blockIdx.x / CL;
+  const long long tstep = gridDim.x / CL;
   if (tile >= ntiles) return;
   Col cur = column(tile);
   if (CF::PREFETCH) prefetch(cur);
   // tiles sharing one pf_bytes-wide row segment; each prefetches N/GT rows
   const int GT = prm.pf_ahead > 0 ? prm.pf_bytes / (B * (int)sizeof(cx<T>)) : 1;
-  for (; tile < ntiles; tile += gridDim.x) {
+  for (; tile < ntiles; tile += tstep) {
+    if constexpr (CL > 1 && TFFFT_COLCLUSTER_SYNC) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+    }
     if (prm.pf_ahead > 0) {
       const long long tp = tile + prm.pf_ahead;
       const int rows = SH::N / GT;
@@ -232,7 +250,7 @@ col_fft_kernel(const ColParams prm) {
     }
     cx<T> v[E];
     Col next = cur;
-    const long long nxt = tile + gridDim.x;
+    const long long nxt = tile + tstep;
     if constexpr (CF::PREFETCH) {
       cp_wait_all();
 #pragma unroll

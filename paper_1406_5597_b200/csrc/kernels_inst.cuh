@@ -37,11 +37,29 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CF::THREADS, sm);
     return n < 1 ? 1 : n;
   }();
-  const long long tiles = (p.ncols + CF::B - 1) / CF::B;
+  const long long tiles = (p.ncols + CF::CL * CF::B - 1) / (CF::CL * CF::B);
   if (tiles <= 0) return cudaSuccess;
-  const long long blocks = CF::PERSISTENT ? std::min<long long>(tiles, (long long)per_sm * num_sms()) : tiles;
+  long long blocks = CF::PERSISTENT ? std::min<long long>(tiles * CF::CL, (long long)per_sm * num_sms())
+                                    : tiles * CF::CL;
+  blocks = std::max<long long>(CF::CL, blocks / CF::CL * CF::CL);
   (void)cudaGetLastError();  // clear any stale error of this thread
-  k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
+  if constexpr (CF::CL == 1) {
+    k<<<(unsigned)blocks, CF::THREADS, sm, s>>>(p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(CF::THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CF::CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, p);
+  }
   return cudaGetLastError();
 }
 
