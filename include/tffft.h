@@ -72,7 +72,10 @@ int tffft_comm_destroy(tffft_comm_t comm);
 
 /* --- plans -------------------------------------------------------------- */
 /* n0, n1, n2: powers of two in [2, 4096]; p = comm size must divide n0 and n1
- * (layout.py:83-93).  pattern: TFFFT_PAIRWISE (chunk-granular in-place landing). */
+ * (layout.py:83-93).  pattern (transport.py:359-419): TFFFT_PAIRWISE = one send
+ * and one receive per peer in one NCCL group; TFFFT_COLLECTIVE = one
+ * ncclAlltoAll over the p-band staging/landing buffers (grouped send/recv when
+ * the loaded NCCL predates 2.28).  Both give bitwise-identical spectra. */
 int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm_t comm,
                       tffft_plan_t* plan);
 /* algorithm flags for tffft_plan_create_ex (0 = the default kernels) */

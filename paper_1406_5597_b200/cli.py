@@ -29,7 +29,7 @@ from .dfft import forward, gather_real, gather_spectral, inverse, plan, scatter_
 from .errors import ConfigurationError, SlabFftError
 from .exchange import Strategy
 from .layout import GlobalGrid, RealSlab, SpectralSlab, validate
-from .transport import run_spmd
+from .transport import CommPattern, run_spmd
 
 MAX_VERIFY_SIZE = 32  # cli.py:30
 ROUNDTRIP_RTOL = 1e-12  # cli.py:49
@@ -97,14 +97,14 @@ def _parse_strategies(text: str) -> list[Strategy]:
 
 
 def _run_pipeline(grid: GlobalGrid, p: int, field: torch.Tensor, iters: int = 0, warmup: int = 0,
-                  strategy: Strategy = Strategy.STRIDED):
+                  strategy: Strategy = Strategy.STRIDED, pattern: CommPattern = CommPattern.PAIRWISE):
     """forward (+ inverse pairs when timing) on p ranks; returns the gathered
     spectrum, per-iteration records (wall us, stage dict, counters) merged
     over ranks, and the worst round-trip relative rms (cli.py:87-128)."""
     slabs = scatter_real(field, grid, p)
 
     def body(ep):
-        fp = plan(grid, ep, strategy, check_consistency=True)
+        fp = plan(grid, ep, strategy, pattern, check_consistency=True)
         fp.enable_timing(True)
         mine = slabs[ep.rank]
         recs = []
@@ -162,7 +162,7 @@ def cmd_verify(args) -> int:
                 continue
             spectra = {}
             for strategy in args.strategies:
-                gathered, _, rel = _run_pipeline(grid, p, field, strategy=strategy)
+                gathered, _, rel = _run_pipeline(grid, p, field, strategy=strategy, pattern=args.comm)
                 spectra[strategy] = gathered
                 for name, err, tol in (("oracle_equivalence", float(abs(gathered - ref).max()), ORACLE_ATOL),
                                        ("round_trip", rel, ROUNDTRIP_RTOL)):
@@ -182,19 +182,19 @@ def cmd_verify(args) -> int:
 
 def _bench_rows(grid: GlobalGrid, p: int, strategy: Strategy, args) -> list[dict]:
     field = _random_field(grid, args.seed)
-    _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
+    _, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy, args.comm)
     if rel > ROUNDTRIP_RTOL:
         raise SlabFftError(f"embedded correctness cross-check failed: round-trip error {rel:.3e} "
                            f"exceeds {ROUNDTRIP_RTOL:.1e} on {grid.n0}x{grid.n1}x{grid.n2}, p={p}")
     rows = []
     for it, (wall, st, cnt) in enumerate(merged):
         rows.append({"grid_n0": grid.n0, "grid_n1": grid.n1, "grid_n2": grid.n2, "p": p,
-                     "strategy": strategy.value, "comm_pattern": "pairwise", "iter": it,
+                     "strategy": strategy.value, "comm_pattern": args.comm.value, "iter": it,
                      "t_total_us": f"{wall:.3f}", "t_stage1_us": f"{st['stage1_us']:.3f}",
                      "t_exchange_us": f"{st['exchange_us']:.3f}", "t_stage3_us": f"{st['stage3_us']:.3f}",
                      "bytes_packed": cnt[0], "bytes_wire": cnt[1], "bytes_unpacked": cnt[2]})
     med = statistics.median(float(r["t_total_us"]) for r in rows)
-    print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  {strategy.value}  comm=pairwise  mode=threaded  "
+    print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  {strategy.value}  comm={args.comm.value}  mode={args.mode}  "
           f"iters={args.iters}  median pair {med:.1f} us", file=sys.stderr)
     return rows
 
@@ -230,11 +230,11 @@ def cmd_compare(args) -> int:
         validate(grid, p)
         res = {}
         for strategy in (Strategy.STRIDED, Strategy.TRANSPOSE):
-            gathered, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy)
+            gathered, merged, rel = _run_pipeline(grid, p, field, args.iters, args.warmup, strategy, args.comm)
             if rel > ROUNDTRIP_RTOL:
                 raise SlabFftError(f"round-trip error {rel:.3e} exceeds {ROUNDTRIP_RTOL:.1e} for {strategy.value}")
             res[strategy] = (gathered, merged)
-        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  comm=pairwise  mode=threaded  iters={args.iters}")
+        print(f"grid {grid.n0}x{grid.n1}x{grid.n2}  p={p}  comm={args.comm.value}  mode={args.mode}  iters={args.iters}")
         print(f"{'strategy':10s} {'t_total_us(med)':>16s} {'t_exchange_us(med)':>19s} "
               f"{'packed':>12s} {'wire':>12s} {'unpacked':>12s}")
         totals = {}
@@ -258,6 +258,18 @@ def cmd_compare(args) -> int:
     return status
 
 
+def _add_common(sub, default_mode: str) -> None:
+    """--comm / --mode / --seed as in cli.py:390-396.  --mode is accepted for
+    command-line compatibility only: GPU ranks always run as concurrent host
+    threads (the reference's SERIAL turnstile is a scheduling device of its
+    simulated fabric)."""
+    sub.add_argument("--comm", type=CommPattern, choices=list(CommPattern), default=CommPattern.PAIRWISE,
+                     help="all-to-all pattern: pairwise or collective (default pairwise)")
+    sub.add_argument("--mode", choices=["threaded", "serial"], default=default_mode,
+                     help="accepted for compatibility; ranks always run as threads")
+    sub.add_argument("--seed", type=int, default=0)
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_1406_5597_b200",
                                      description="B200 transpose-free slab 3D FFT: verification and benchmarks.")
@@ -267,7 +279,7 @@ def build_parser() -> argparse.ArgumentParser:
     pv.add_argument("--procs", type=_parse_procs, default=[1, 2, 4])
     pv.add_argument("--strategy", dest="strategies", type=_parse_strategies,
                     default=[Strategy.STRIDED, Strategy.TRANSPOSE])
-    pv.add_argument("--seed", type=int, default=0)
+    _add_common(pv, "serial")
     pv.set_defaults(func=cmd_verify)
     pb = sub.add_parser("bench", help="time forward+inverse pairs and emit CSV")
     pb.add_argument("--size", type=_parse_size, required=True)
@@ -276,14 +288,14 @@ def build_parser() -> argparse.ArgumentParser:
     pb.add_argument("--warmup", type=int, default=1)
     pb.add_argument("--output", default=None)
     pb.add_argument("--strategy", dest="strategies", type=_parse_strategies, default=[Strategy.STRIDED])
-    pb.add_argument("--seed", type=int, default=0)
+    _add_common(pb, "threaded")
     pb.set_defaults(func=cmd_bench)
     pc = sub.add_parser("compare", help="run both strategies on identical inputs")
     pc.add_argument("--size", type=_parse_size, required=True)
     pc.add_argument("--procs", type=_parse_procs, default=[4])
     pc.add_argument("--iters", type=int, default=5)
     pc.add_argument("--warmup", type=int, default=1)
-    pc.add_argument("--seed", type=int, default=0)
+    _add_common(pc, "threaded")
     pc.set_defaults(func=cmd_compare)
     return parser
 

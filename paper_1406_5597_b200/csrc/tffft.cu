@@ -80,6 +80,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.28): the COLLECTIVE pattern's single all-to-all
+  ncclResult_t (*AlltoAll)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 static NcclApi& nccl() {
@@ -101,6 +103,7 @@ static NcclApi& nccl() {
     LOAD(GetUniqueId) LOAD(CommInitRank) LOAD(CommDestroy) LOAD(CommAbort) LOAD(CommGetAsyncError)
     LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd) LOAD(GetErrorString)
 #undef LOAD
+    api.AlltoAll = reinterpret_cast<decltype(api.AlltoAll)>(dlsym(h, "ncclAlltoAll"));
     api.loaded = true;
   });
   return api;
@@ -638,6 +641,15 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
     const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
     char* stg = static_cast<char*>(pl->staging);
     char* lnd = static_cast<char*>(pl->landing);
+    if (pl->pattern == TFFFT_COLLECTIVE && api.AlltoAll) {
+      // COLLECTIVE (transport.py:395-419): every rank deposits all of its
+      // outgoing bands in one all-to-all.  Staging and landing hold p bands, so
+      // the self slot travels too (a local copy nobody reads: the self band
+      // stays in the slab).
+      NCCL_TRY(api.AlltoAll(stg, lnd, 2 * band, dt, pl->comm->nccl, s));
+      pl->counters[1] += wire_bytes(pl);
+      return TFFFT_OK;
+    }
     NCCL_TRY(api.GroupStart());
     for (int d = 1; d < pl->p; ++d) {
       const int to = (pl->rank + d) % pl->p, from = (pl->rank - d + pl->p) % pl->p;
@@ -646,6 +658,9 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
     }
     NCCL_TRY(api.GroupEnd());
   } else {
+    // the local fabric's pull is already collective-shaped for both patterns:
+    // every rank deposits (records its staging), waits for all p deposits,
+    // then collects its p-1 incoming bands in one launch
     LocalFabric& fab = *pl->comm->fabric;
     auto& slot = fab.slot(pl->seq);
     CUDA_TRY(cudaEventRecord(slot.ready[pl->rank], s));
@@ -923,8 +938,8 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   if ((long long)(n0 / p) * n1 * (n2 / 2 + 1) >= (1LL << 32))
     return fail(TFFFT_ERR_SIZE, "local slab of %lld complex elements exceeds 2^32; use more ranks",
                 (long long)(n0 / p) * n1 * (n2 / 2 + 1));
-  if (pattern != TFFFT_PAIRWISE)
-    return fail(TFFFT_ERR_CONFIGURATION, "only the PAIRWISE comm pattern is implemented on the GPU");
+  if (pattern != TFFFT_PAIRWISE && pattern != TFFFT_COLLECTIVE)
+    return fail(TFFFT_ERR_CONFIGURATION, "unknown comm pattern %d", pattern);
 
   auto pl = std::make_unique<tffft_plan_s>();
   pl->comm = comm;

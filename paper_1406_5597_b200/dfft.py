@@ -119,6 +119,9 @@ ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8}
 TRANSPOSE_FLAG = 4
 
 
+_PATTERN_CODE = {CommPattern.PAIRWISE: 0, CommPattern.COLLECTIVE: 1}  # TFFFT_PAIRWISE / TFFFT_COLLECTIVE
+
+
 def _spectral_tag(strategy: Strategy) -> SpectralTag:
     return SpectralTag.STRIDED_INPLACE if strategy is Strategy.STRIDED else SpectralTag.CONTIGUOUS_FLIPPED
 
@@ -132,8 +135,8 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     "fourstep_stage3"); None takes the library defaults (TFFFT_FUSE /
     TFFFT_FOURSTEP environment switches)."""
     validate(grid, comm.p)
-    if comm_pattern is not CommPattern.PAIRWISE:
-        raise ConfigurationError("the B200 path implements the PAIRWISE comm pattern only")
+    if not isinstance(comm_pattern, CommPattern):
+        raise ConfigurationError(f"comm_pattern must be a CommPattern, got {comm_pattern!r}")
     if dtype not in DTYPES:
         raise ConfigurationError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
     code, rdt, cdt = DTYPES[dtype]
@@ -147,7 +150,7 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
         flags = (0 if flags < 0 else flags) | TRANSPOSE_FLAG
     h = ctypes.c_void_p()
     with torch.cuda.device(comm.device):
-        _lib.check(_lib.lib().tffft_plan_create_ex(grid.n0, grid.n1, grid.n2, code, 0, flags, comm.handle,
+        _lib.check(_lib.lib().tffft_plan_create_ex(grid.n0, grid.n1, grid.n2, code, _PATTERN_CODE[comm_pattern], flags, comm.handle,
                                                    ctypes.byref(h)))
         p, rank = comm.p, comm.rank
         dev = torch.device("cuda", comm.device)

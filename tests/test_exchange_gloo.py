@@ -26,7 +26,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, shape, q):
+def _worker(rank, world, port, shape, q, pattern="pairwise"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,14 +40,19 @@ def _worker(rank, world, port, shape, q):
         spec, staging = oracle.stage1_band_staging(s1, world, rank)
         stg = torch.from_numpy(staging.reshape(-1).copy())
         landing = torch.zeros_like(stg)
-        ops = tf.exchange_schedule(n0, n1, n2, world, rank)
-        reqs = []
-        for op in ops:  # libtffft posts all sends and receives of a rank in one group
-            reqs.append(dist.isend(stg[op.send_offset:op.send_offset + op.count].clone(), op.peer))
-        for op in ops:
-            reqs.append(dist.irecv(landing[op.recv_offset:op.recv_offset + op.count], op.peer))
-        for r in reqs:
-            r.wait()
+        if pattern == "collective":
+            # TFFFT_COLLECTIVE: one all-to-all over the p-band staging / landing
+            # buffers (the self slot travels but is never read)
+            dist.all_to_all_single(torch.view_as_real(landing), torch.view_as_real(stg))
+        else:
+            ops = tf.exchange_schedule(n0, n1, n2, world, rank)
+            reqs = []
+            for op in ops:  # libtffft posts all sends and receives of a rank in one group
+                reqs.append(dist.isend(stg[op.send_offset:op.send_offset + op.count].clone(), op.peer))
+            for op in ops:
+                reqs.append(dist.irecv(landing[op.recv_offset:op.recv_offset + op.count], op.peer))
+            for r in reqs:
+                r.wait()
         # the stage-3 kernel's read addressing: block s != rank of a column comes
         # from landing[s][i][j][k], the self block from the in-place slab
         n1p, n2c = n1 // world, n2 // 2 + 1
@@ -64,12 +69,13 @@ def _worker(rank, world, port, shape, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("pattern", ["pairwise", "collective"])
 @pytest.mark.parametrize("world,shape", [(2, (8, 8, 8)), (2, (16, 4, 32)), (4, (8, 16, 4))])
-def test_exchange_schedule_over_gloo(world, shape):
+def test_exchange_schedule_over_gloo(world, shape, pattern):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, q, pattern)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -61,7 +61,7 @@ def test_real_scatter_gather():
         tf.RealSlab(slabs[0].layout, torch.zeros(32, dtype=torch.int32))
 
 
-def test_plan_rejects_collective_pattern_without_gpu():
+def test_plan_rejects_unknown_comm_pattern_without_gpu():
     with pytest.raises(tf.ConfigurationError):
         tf.plan(tf.GlobalGrid(8, 8, 8), type("E", (), {"p": 1, "rank": 0})(), tf.Strategy.STRIDED,
-                tf.CommPattern.COLLECTIVE)
+                "collective")

@@ -98,8 +98,8 @@ def test_plan_create_validates_before_touching_the_gpu():
             _lib.check(lib.tffft_plan_create(n0, n1, n2, 0, 0, arr[0], ctypes.byref(h)))
     with pytest.raises(tf.ConfigurationError):  # unknown dtype
         _lib.check(lib.tffft_plan_create(8, 8, 8, 7, 0, arr[0], ctypes.byref(h)))
-    with pytest.raises(tf.ConfigurationError):  # COLLECTIVE pattern not on the GPU path
-        _lib.check(lib.tffft_plan_create(8, 8, 8, 0, 1, arr[0], ctypes.byref(h)))
+    with pytest.raises(tf.ConfigurationError):  # unknown comm pattern
+        _lib.check(lib.tffft_plan_create(8, 8, 8, 0, 7, arr[0], ctypes.byref(h)))
     for r in range(2):
         lib.tffft_comm_destroy(arr[r])
 
