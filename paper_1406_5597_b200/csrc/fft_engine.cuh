@@ -317,14 +317,21 @@ struct Stockham {
     }
   }
 
-  template <int p>
-  static __device__ __forceinline__ void rest(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
+  // hook() runs once the last exchange has drained the buffer (every thread
+  // has loaded its operands of the last pass), before that pass computes
+  template <int p, class Hook>
+  static __device__ __forceinline__ void rest(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw,
+                                              Hook& hook) {
     if constexpr (p < P) {
       exchange<p>(sm, v, tt, b);
+      if constexpr (p == P - 1) hook();
       compute<p>(v, tt, tw);
-      rest<p + 1>(sm, v, tt, b, tw);
+      rest<p + 1>(sm, v, tt, b, tw, hook);
     }
   }
+  struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+  };
 
   // v holds pass-0 inputs (element in_elem(tt,u,m) in v[u*R0+m]); on return
   // v[u*RL+m] holds output element out_elem(tt,u,m).  All threads of the CTA
@@ -333,7 +340,13 @@ struct Stockham {
     if constexpr (P > 0) compute<0>(v, tt, tw);
   }
   static __device__ __forceinline__ void finish(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
-    if constexpr (P > 0) rest<1>(sm, v, tt, b, tw);
+    NoHook h;
+    if constexpr (P > 0) rest<1>(sm, v, tt, b, tw, h);
+  }
+  template <class Hook>
+  static __device__ __forceinline__ void finish(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw,
+                                                Hook& hook) {
+    if constexpr (P > 0) rest<1>(sm, v, tt, b, tw, hook);
   }
   static __device__ __forceinline__ void run(void* sm, cx<T>* v, int tt, int b, const cx<T>* __restrict__ tw) {
     first(v, tt, tw);
