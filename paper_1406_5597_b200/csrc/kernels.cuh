@@ -48,7 +48,7 @@ struct RowParams {
   int n2c;
   int rows_per_plane;
   double scale;                   // c2r output scale
-  unsigned long long* stats;      // c2r: per plane [m2, edge, residue] as ordered doubles
+  double* row_stats;              // c2r: per row [max |X|^2, max |Im X_0|,|Im X_N|, |Im X_0|+|Im X_N|]
 };
 
 // Column CTA: B adjacent columns, TPT threads per column, E elements per
@@ -157,6 +157,10 @@ template <int L> struct RowCfg {
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;  // one pad slot per E elements
   static constexpr int N = Shape<L>::N;
   static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
+  // c2r at n2 = 1024: the consistency statistics lift the kernel to 111
+  // registers (4 CTAs of 128 threads per SM); asking for 5 keeps it at 96 with
+  // no spills, like r2c.  Other lengths spill under that cap and keep the default.
+  static constexpr int MINB_C2R = (L == 9 && THREADS == 128) ? 5 : TFFFT_ROW_MINB;
 };
 
 template <typename T, int L, bool WIDE = false>
@@ -389,7 +393,7 @@ r2c_rows_kernel(const RowParams prm) {
 __device__ __forceinline__ unsigned long long ord(double x) { return __double_as_longlong(x); }
 
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, TFFFT_ROW_MINB)
+__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::MINB_C2R)
 c2r_rows_kernel(const RowParams prm) {
   using RC = RowCfg<L>;
   using SH = Shape<L>;
@@ -407,8 +411,14 @@ c2r_rows_kernel(const RowParams prm) {
   const cx<T>* in = reinterpret_cast<const cx<T>*>(prm.spec) + (valid ? row : 0) * prm.n2c;
 
   // row -> shared memory, with the statistics of the Hermitian check: max |X|^2
-  // over the row (every thread), |Im X_0|, |Im X_N| (thread tt == 0 only)
-  double m2 = 0.0;
+  // over the row (every thread), |Im X_0|, |Im X_N| (thread tt == 0 only).
+  // Each row writes one plain 24-byte record (reduced per plane on request by
+  // reduce_row_stats_kernel): atomics from the ~1000 rows of a plane in flight
+  // would serialise on a few L2 addresses (measured +0.4 ms per 1024^3 launch).
+  constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
+  constexpr int SEGS = SH::TPT / W;  // warp segments per row
+  __shared__ double seg_m2[RC::B][SEGS];
+  double m2 = 0.0, e0 = 0.0, eN = 0.0;
 #pragma unroll
   for (int q = 0; q < SH::E; ++q) {
     const int k = tt + SH::TPT * q;
@@ -420,23 +430,25 @@ c2r_rows_kernel(const RowParams prm) {
     cx<T> X0 = sm[ST::sidx(b, 0)];
     cx<T> XN = in[N];
     m2 = fmax(m2, fma((double)XN.x, (double)XN.x, (double)XN.y * XN.y));
-    const double e0 = fabs((double)X0.y), eN = fabs((double)XN.y);
-    if (valid && prm.stats != nullptr) {
-      unsigned long long* st = prm.stats + 3 * (row / prm.rows_per_plane);
-      atomicMax(st + 1, ord(fmax(e0, eN)));
-      atomicMax(st + 2, ord(e0 + eN));
-    }
+    e0 = fabs((double)X0.y);
+    eN = fabs((double)XN.y);
     X0.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
     XN.y = T(0);
     sm[ST::sidx(b, 0)] = X0;
     sm[ST::sidx(b, N)] = XN;
   }
-  constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o, W));
-  if (valid && prm.stats != nullptr && (tt % W) == 0)
-    atomicMax(prm.stats + 3 * (row / prm.rows_per_plane), ord(m2));
+  if ((tt % W) == 0) seg_m2[b][tt / W] = m2;
   __syncthreads();
+  if (tt == 0 && valid && prm.row_stats != nullptr) {
+#pragma unroll
+    for (int g = 1; g < SEGS; ++g) m2 = fmax(m2, seg_m2[b][g]);
+    double* rec = prm.row_stats + 3 * row;
+    rec[0] = m2;
+    rec[1] = fmax(e0, eN);
+    rec[2] = e0 + eN;
+  }
 
   cx<T> v[SH::E];
 #pragma unroll
@@ -466,6 +478,31 @@ c2r_rows_kernel(const RowParams prm) {
       const cx<T> z = v[u * SH::RL + m];
       outc[SH::out_elem(tt, u, m)] = cx<T>{z.x * s, z.y * s};
     }
+}
+
+// per-plane maxima of the c2r row records (one CTA per plane), stored as the
+// ordered-double words the host check reads (same format as the fused
+// kernel's atomics)
+static __global__ void __launch_bounds__(256) reduce_row_stats_kernel(const double* rec, int rows_per_plane,
+                                                               unsigned long long* out) {
+  const long long base = (long long)blockIdx.x * rows_per_plane;
+  double m[3] = {0.0, 0.0, 0.0};
+  for (int r = threadIdx.x; r < rows_per_plane; r += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m[c] = fmax(m[c], rec[3 * (base + r) + c]);
+  __shared__ double red[3][8];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m[c] = fmax(m[c], __shfl_xor_sync(0xffffffffu, m[c], o));
+    if (threadIdx.x % 32 == 0) red[c][threadIdx.x / 32] = m[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) v = fmax(v, red[threadIdx.x][w]);
+    out[3 * blockIdx.x + threadIdx.x] = ord(v);
+  }
 }
 
 // host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)

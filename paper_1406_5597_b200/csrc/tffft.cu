@@ -209,7 +209,8 @@ struct tffft_plan_s {
   void* tw1 = nullptr;
   void* tw2 = nullptr;
   void* tw2post = nullptr;
-  unsigned long long* stats = nullptr;
+  unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles)
+  double* row_stats = nullptr;          // per row records of the c2r kernel
   void** pull_ptrs = nullptr;  // local fabric: device array [2 * nchunks] of (src, dst)
   // stage-3 four-step (fourstep.cuh): L2-resident scratch ring, counters, tables
   int fs_la = 0, fs_G = 0, fs_groups = 0;
@@ -537,7 +538,7 @@ static RowParams row_params(tffft_plan_t pl, void* real, void* spec) {
   r.n2c = pl->n2c;
   r.rows_per_plane = pl->n1;
   r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
-  r.stats = pl->stats;
+  r.row_stats = pl->row_stats;
   return r;
 }
 
@@ -959,6 +960,8 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
   CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
   ws += sizeof(unsigned long long) * 3 * pl->n0p;
+  CUDA_TRY(cudaMalloc(&pl->row_stats, sizeof(double) * 3 * (size_t)pl->n0p * pl->n1));
+  ws += sizeof(double) * 3 * (size_t)pl->n0p * pl->n1;
   if (p == 1 && strategy == 1) {  // TRANSPOSE packs even on one rank (exchange.py:195-219)
     const size_t sb = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
     CUDA_TRY(cudaMalloc(&pl->staging, sb));
@@ -1045,7 +1048,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaSetDevice(pl->comm->device);
   free_events(pl);
   cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
-  cudaFree(pl->stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
+  cudaFree(pl->stats); cudaFree(pl->row_stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
   cudaFree(pl->band_dst);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
@@ -1121,7 +1124,8 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   CUDA_TRY(cudaSetDevice(pl->comm->device));
   StageEvents* ev;
   TRY(begin_events(pl, false, s, &ev));
-  CUDA_TRY(cudaMemsetAsync(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p, s));
+  if (pl->s1_fused)  // the fused kernel max-reduces into the per-plane statistics
+    CUDA_TRY(cudaMemsetAsync(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p, s));
   // stage 3' (dfft.py:196-197)
   TRY(fabric_guard_staging(pl, s));
   if (pl->strategy == 1) {
@@ -1201,6 +1205,10 @@ int tffft_consistency(tffft_plan_t pl, double* residue) {
   *residue = 0.0;
   if (!pl->inverse_ran) return TFFFT_OK;
   CUDA_TRY(cudaSetDevice(pl->comm->device));
+  if (!pl->s1_fused) {  // fold the c2r row records into per-plane maxima
+    reduce_row_stats_kernel<<<pl->n0p, 256, 0, pl->last_inverse_stream>>>(pl->row_stats, pl->n1, pl->stats);
+    CUDA_TRY(cudaGetLastError());
+  }
   CUDA_TRY(cudaStreamSynchronize(pl->last_inverse_stream));
   std::vector<double> st(3 * (size_t)pl->n0p);
   CUDA_TRY(cudaMemcpy(st.data(), pl->stats, st.size() * sizeof(double), cudaMemcpyDeviceToHost));
