@@ -150,6 +150,12 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #ifndef TFFFT_ROW_MINB
 #define TFFFT_ROW_MINB 1
 #endif
+#ifndef TFFFT_C2R_MINB9
+#define TFFFT_C2R_MINB9 6
+#endif
+#ifndef TFFFT_R2C_MINB9
+#define TFFFT_R2C_MINB9 6
+#endif
 template <int L> struct RowCfg {
   static constexpr int TPT = Shape<L>::TPT;
   static constexpr int B = TFFFT_ROW_THREADS / TPT > 1 ? TFFFT_ROW_THREADS / TPT : 1;
@@ -157,10 +163,13 @@ template <int L> struct RowCfg {
   static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;  // one pad slot per E elements
   static constexpr int N = Shape<L>::N;
   static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
-  // c2r at n2 = 1024: the consistency statistics lift the kernel to 111
-  // registers (4 CTAs of 128 threads per SM); asking for 5 keeps it at 96 with
-  // no spills, like r2c.  Other lengths spill under that cap and keep the default.
-  static constexpr int MINB_C2R = (L == 9 && THREADS == 128) ? 5 : TFFFT_ROW_MINB;
+  // n2 = 1024 row kernels: r2c would take 93 and c2r (with its consistency
+  // statistics) 111 registers, i.e. 5 / 4 CTAs of 128 threads per SM; asking
+  // for 6 CTAs caps both at 80 registers with no spills (measured best of 5 / 6
+  // / 8: c2r 3.54 -> 3.47 ms, r2c 3.17 -> 3.10 ms per 1024^3 launch).  Other
+  // lengths spill under such caps and keep the default.
+  static constexpr int MINB_C2R = (L == 9 && THREADS == 128) ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
+  static constexpr int MINB_R2C = (L == 9 && THREADS == 128) ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
 };
 
 template <typename T, int L, bool WIDE = false>
@@ -336,7 +345,7 @@ col_fft_kernel(const ColParams prm) {
 // r2c along n2 (packed: n2 reals -> N = n2/2 complex FFT -> n2/2+1 bins)
 // ---------------------------------------------------------------------------
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, TFFFT_ROW_MINB)
+__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::MINB_R2C)
 r2c_rows_kernel(const RowParams prm) {
   using RC = RowCfg<L>;
   using SH = Shape<L>;
