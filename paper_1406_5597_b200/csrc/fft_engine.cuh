@@ -28,9 +28,15 @@ namespace tffft {
 // ---------------------------------------------------------------------------
 constexpr int kMaxRadixBits = 4;
 constexpr int kMaxLog = 12;
+#ifndef TFFFT_L10_RADIX_BITS
+#define TFFFT_L10_RADIX_BITS 5
+#endif
+// largest radix (bits) of a length-2^L schedule; E = 2^(first radix bits)
+// operands per thread
+__host__ __device__ constexpr int max_radix_bits(int L) { return L == 10 ? TFFFT_L10_RADIX_BITS : kMaxRadixBits; }
 
 __host__ __device__ constexpr int num_passes(int L) {
-  return L == 0 ? 0 : (L + kMaxRadixBits - 1) / kMaxRadixBits;
+  return L == 0 ? 0 : (L + max_radix_bits(L) - 1) / max_radix_bits(L);
 }
 __host__ __device__ constexpr int pass_bits(int L, int p) {
   return (L / num_passes(L)) + (p < (L % num_passes(L)) ? 1 : 0);
@@ -144,9 +150,33 @@ __device__ __forceinline__ cx<T> mul_w16(cx<T> a, int t) {
   return {fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s)};
 }
 
+// exp(-2*pi*i*t/32), t < 16 (even t via mul_w16)
+template <bool INV, typename T>
+__device__ __forceinline__ cx<T> mul_w32(cx<T> a, int t) {
+  if ((t & 1) == 0) return mul_w16<INV>(a, t >> 1);
+  const T k1 = T(0.980785280403230449126182236134239037);
+  const T k3 = T(0.831469612302545237078788377617905756);
+  const T k5 = T(0.555570233019602224742830813948532874);
+  const T k7 = T(0.195090322016128267848284868477022240);
+  T c, s;
+  switch (t & 15) {
+    case 1: c = k1; s = k7; break;
+    case 3: c = k3; s = k5; break;
+    case 5: c = k5; s = k3; break;
+    case 7: c = k7; s = k1; break;
+    case 9: c = -k7; s = k1; break;
+    case 11: c = -k5; s = k3; break;
+    case 13: c = -k3; s = k5; break;
+    default: c = -k1; s = k7; break;  // 15
+  }
+  if (INV) s = -s;
+  return {fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s)};
+}
+
 template <int R, bool INV, typename T>
 struct DFT {
   static __device__ __forceinline__ void run(cx<T>* a) {
+    static_assert(R <= 32, "radix above 32");
     constexpr int H = R / 2;
     cx<T> e[H], o[H];
 #pragma unroll
@@ -155,7 +185,7 @@ struct DFT {
     DFT<H, INV, T>::run(o);
 #pragma unroll
     for (int k = 0; k < H; ++k) {
-      cx<T> t = mul_w16<INV>(o[k], k * (16 / R));
+      cx<T> t = mul_w32<INV>(o[k], k * (32 / R));
       a[k] = cadd(e[k], t);
       a[k + H] = csub(e[k], t);
     }
