@@ -62,6 +62,8 @@ GRIDS = [
     ((64, 64, 64), 1), ((32, 64, 128), 4), ((128, 16, 32), 8), ((16, 256, 64), 2),
     ((8, 8, 2048), 1), ((8, 2048, 4), 2), ((2048, 4, 8), 4), ((4096, 2, 2), 1), ((2, 4096, 4), 2),
     ((4, 4, 4096), 1), ((512, 8, 16), 8),
+    # 1024-point transforms (two radix-32 passes) on every axis and path
+    ((1024, 8, 16), 1), ((16, 1024, 8), 1), ((4, 8, 2048), 1), ((1024, 1024, 4), 2), ((1024, 16, 1024), 4),
 ]
 
 
@@ -165,6 +167,7 @@ ALG_CASES = [
     ((1024, 8, 8), 1, ("fourstep_stage3",)),      # TMA-fed four-step (p = 1)
     ((1024, 16, 64), 1, ("fourstep_stage3",)),
     ((8, 1024, 1024), 2, ("fused_stage1",)),
+    ((2, 1024, 1024), 1, ("fused_stage1",)),
 ]
 
 
