@@ -33,7 +33,12 @@ constexpr int kMaxLog = 12;
 #endif
 // largest radix (bits) of a length-2^L schedule; E = 2^(first radix bits)
 // operands per thread
-__host__ __device__ constexpr int max_radix_bits(int L) { return L == 10 ? TFFFT_L10_RADIX_BITS : kMaxRadixBits; }
+#ifndef TFFFT_L9_RADIX_BITS
+#define TFFFT_L9_RADIX_BITS 5
+#endif
+__host__ __device__ constexpr int max_radix_bits(int L) {
+  return L == 10 ? TFFFT_L10_RADIX_BITS : L == 9 ? TFFFT_L9_RADIX_BITS : kMaxRadixBits;
+}
 
 __host__ __device__ constexpr int num_passes(int L) {
   return L == 0 ? 0 : (L + max_radix_bits(L) - 1) / max_radix_bits(L);

@@ -168,8 +168,10 @@ template <int L> struct RowCfg {
   // for 6 CTAs caps both at 80 registers with no spills (measured best of 5 / 6
   // / 8: c2r 3.54 -> 3.47 ms, r2c 3.17 -> 3.10 ms per 1024^3 launch).  Other
   // lengths spill under such caps and keep the default.
-  static constexpr int MINB_C2R = (L == 9 && THREADS == 128) ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
-  static constexpr int MINB_R2C = (L == 9 && THREADS == 128) ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
+  // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
+  static constexpr bool CAP = L == 9 && THREADS == 128 && Shape<L>::E == 8;
+  static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
+  static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
 };
 
 template <typename T, int L, bool WIDE = false>

@@ -43,11 +43,11 @@ def test_radix_schedule_matches_design():
         prod = 1
         for x in got[L]:
             prod *= x
-            assert x <= (32 if L == 10 else 16)
+            assert x <= (32 if L in (9, 10) else 16)
         assert prod == 1 << L
-    # 1024-point transforms (the headline columns) run as two radix-32 passes:
-    # one shared-memory exchange instead of two
-    assert got[10] == [32, 32] and got[9] == [8, 8, 8] and got[11] == [16, 16, 8]
+    # 512- and 1024-point transforms (the headline rows and columns) run as two
+    # radix-32/16 passes: one shared-memory exchange instead of two
+    assert got[10] == [32, 32] and got[9] == [32, 16] and got[11] == [16, 16, 8]
 
 
 @pytest.mark.parametrize("n0,n1,n2,p", [(4, 4, 2, 2), (8, 8, 8, 4), (16, 8, 32, 8), (128, 128, 128, 2)])
