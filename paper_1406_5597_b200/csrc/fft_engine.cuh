@@ -40,23 +40,28 @@ __host__ __device__ constexpr int max_radix_bits(int L) {
   return L == 10 ? TFFFT_L10_RADIX_BITS : L == 9 ? TFFFT_L9_RADIX_BITS : kMaxRadixBits;
 }
 
-__host__ __device__ constexpr int num_passes(int L) {
-  return L == 0 ? 0 : (L + max_radix_bits(L) - 1) / max_radix_bits(L);
+// Every schedule function takes an optional mb = largest radix in bits
+// (default: max_radix_bits(L)); a kernel may run its own schedule, see
+// r2c_radix_bits in kernels.cuh.  The host table builder uses the same functions.
+__host__ __device__ constexpr int sched_bits(int L, int mb) { return mb > 0 ? mb : max_radix_bits(L); }
+__host__ __device__ constexpr int num_passes(int L, int mb = 0) {
+  return L == 0 ? 0 : (L + sched_bits(L, mb) - 1) / sched_bits(L, mb);
 }
-__host__ __device__ constexpr int pass_bits(int L, int p) {
-  return (L / num_passes(L)) + (p < (L % num_passes(L)) ? 1 : 0);
+__host__ __device__ constexpr int pass_bits(int L, int p, int mb = 0) {
+  return (L / num_passes(L, mb)) + (p < (L % num_passes(L, mb)) ? 1 : 0);
 }
-__host__ __device__ constexpr int ept_bits(int L) { return L == 0 ? 0 : pass_bits(L, 0); }
-__host__ __device__ constexpr int ns_bits(int L, int p) {
-  return p == 0 ? 0 : ns_bits(L, p - 1) + pass_bits(L, p - 1);
+__host__ __device__ constexpr int ept_bits(int L, int mb = 0) { return L == 0 ? 0 : pass_bits(L, 0, mb); }
+__host__ __device__ constexpr int ns_bits(int L, int p, int mb = 0) {
+  return p == 0 ? 0 : ns_bits(L, p - 1, mb) + pass_bits(L, p - 1, mb);
 }
 // offset of pass p's twiddle block (passes >= 1 only); block p holds the Ns
 // roots exp(-2 pi i k / (Ns R)), k < Ns; powers m = 2..R-1 are formed in registers
-__host__ __device__ constexpr int tw_offset(int L, int p) {
-  return p <= 1 ? 0 : tw_offset(L, p - 1) + (1 << ns_bits(L, p - 1));
+__host__ __device__ constexpr int tw_offset(int L, int p, int mb = 0) {
+  return p <= 1 ? 0 : tw_offset(L, p - 1, mb) + (1 << ns_bits(L, p - 1, mb));
 }
-__host__ __device__ constexpr int tw_total(int L) {
-  return num_passes(L) <= 1 ? 0 : tw_offset(L, num_passes(L) - 1) + (1 << ns_bits(L, num_passes(L) - 1));
+__host__ __device__ constexpr int tw_total(int L, int mb = 0) {
+  return num_passes(L, mb) <= 1 ? 0
+                                : tw_offset(L, num_passes(L, mb) - 1, mb) + (1 << ns_bits(L, num_passes(L, mb) - 1, mb));
 }
 
 // ---------------------------------------------------------------------------
@@ -243,16 +248,16 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 // ---------------------------------------------------------------------------
 // Stockham pass machinery
 // ---------------------------------------------------------------------------
-template <int L>
+template <int L, int MB = 0>
 struct Shape {
   static constexpr int N = 1 << L;
-  static constexpr int P = num_passes(L);
-  static constexpr int EB = ept_bits(L);
+  static constexpr int P = num_passes(L, MB);
+  static constexpr int EB = ept_bits(L, MB);
   static constexpr int E = 1 << EB;
   static constexpr int TPT = N / E;  // threads per transform
-  static constexpr int R0 = L == 0 ? 1 : (1 << pass_bits(L, 0));
-  static constexpr int RL = L == 0 ? 1 : (1 << pass_bits(L, P - 1));
-  static constexpr int TW = tw_total(L);
+  static constexpr int R0 = L == 0 ? 1 : (1 << pass_bits(L, 0, MB));
+  static constexpr int RL = L == 0 ? 1 : (1 << pass_bits(L, P - 1, MB));
+  static constexpr int TW = tw_total(L, MB);
   // element index held in v[u*R0+m] before pass 0 / in v[u*RL+m] after the last pass
   static __device__ __forceinline__ int in_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / R0); }
   static __device__ __forceinline__ int out_elem(int tt, int u, int m) { return tt + TPT * u + m * (N / RL); }
@@ -266,29 +271,29 @@ struct Shape {
 // SYNC: 0 = __syncthreads; 32 = __syncwarp (every transform inside one warp);
 // otherwise the CTA is split into independent groups of SYNC threads and group
 // g = tid / SYNC synchronises on named barrier 1 + g.
-template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0, bool TWS = false>
+template <typename T, int L, bool INV, int S, int PS, bool SPLIT = false, int SYNC = 0, bool TWS = false, int MB = 0>
 struct Stockham {
   static __device__ __forceinline__ void sync() {
     if constexpr (SYNC == 0) __syncthreads();
     else if constexpr (SYNC == 32) __syncwarp();
     else asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / SYNC), "n"(SYNC) : "memory");
   }
-  using SH = Shape<L>;
+  using SH = Shape<L, MB>;
   static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT, P = SH::P;
 
   static __device__ __forceinline__ int sidx(int b, int a) { return b * S + a + (a >> PS); }
 
   template <int p>
   static __device__ __forceinline__ void compute(cx<T>* v, int tt, const cx<T>* __restrict__ tw) {
-    constexpr int R = 1 << pass_bits(L, p);
-    constexpr int NS = 1 << ns_bits(L, p);
+    constexpr int R = 1 << pass_bits(L, p, MB);
+    constexpr int NS = 1 << ns_bits(L, p, MB);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       if constexpr (p > 0) {
         const int j = tt + TPT * u;
         const int k = j & (NS - 1);
         cx<T> pw[R];
-        twiddle_powers<R>(tw_cx<TWS>(tw + tw_offset(L, p) + k), pw);
+        twiddle_powers<R>(tw_cx<TWS>(tw + tw_offset(L, p, MB) + k), pw);
 #pragma unroll
         for (int m = 1; m < R; ++m) v[u * R + m] = ctw<INV>(v[u * R + m], pw[m]);
       }
@@ -311,8 +316,8 @@ struct Stockham {
 
   template <int p, int COMP>
   static __device__ __forceinline__ void store(void* sm, const cx<T>* v, int tt, int b) {
-    constexpr int R = 1 << pass_bits(L, p);
-    constexpr int NS = 1 << ns_bits(L, p);
+    constexpr int R = 1 << pass_bits(L, p, MB);
+    constexpr int NS = 1 << ns_bits(L, p, MB);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       const int j = tt + TPT * u;
@@ -324,7 +329,7 @@ struct Stockham {
 
   template <int p, int COMP>
   static __device__ __forceinline__ void load(const void* sm, cx<T>* v, int tt, int b) {
-    constexpr int R = 1 << pass_bits(L, p);
+    constexpr int R = 1 << pass_bits(L, p, MB);
 #pragma unroll
     for (int u = 0; u < E / R; ++u) {
       const int j = tt + TPT * u;

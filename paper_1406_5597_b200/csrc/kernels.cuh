@@ -156,12 +156,22 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #ifndef TFFFT_R2C_MINB9
 #define TFFFT_R2C_MINB9 6
 #endif
-template <int L> struct RowCfg {
-  static constexpr int TPT = Shape<L>::TPT;
+// r2c row schedule: float64 rows of n2 = 1024 run the radix-8 schedule
+// (3 passes, E = 8, 6 CTAs/SM: 3.10 ms per 1024^3 launch vs 3.62 ms with radix
+// 32x16); every other row / column transform uses the default schedule
+#ifndef TFFFT_R2C_L9_F64_MB
+#define TFFFT_R2C_L9_F64_MB 4
+#endif
+__host__ __device__ constexpr int r2c_radix_bits(int L, int real_bytes) {
+  return (L == 9 && real_bytes == 8) ? TFFFT_R2C_L9_F64_MB : 0;
+}
+
+template <int L, int MB = 0> struct RowCfg {
+  static constexpr int TPT = Shape<L, MB>::TPT;
   static constexpr int B = TFFFT_ROW_THREADS / TPT > 1 ? TFFFT_ROW_THREADS / TPT : 1;
   static constexpr int THREADS = TPT * B;
-  static constexpr int PS = Shape<L>::EB > 0 ? Shape<L>::EB : 30;  // one pad slot per E elements
-  static constexpr int N = Shape<L>::N;
+  static constexpr int PS = Shape<L, MB>::EB > 0 ? Shape<L, MB>::EB : 30;  // one pad slot per E elements
+  static constexpr int N = Shape<L, MB>::N;
   static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
   // n2 = 1024 row kernels: r2c would take 93 and c2r (with its consistency
   // statistics) 111 registers, i.e. 5 / 4 CTAs of 128 threads per SM; asking
@@ -169,7 +179,7 @@ template <int L> struct RowCfg {
   // / 8: c2r 3.54 -> 3.47 ms, r2c 3.17 -> 3.10 ms per 1024^3 launch).  Other
   // lengths spill under such caps and keep the default.
   // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
-  static constexpr bool CAP = L == 9 && THREADS == 128 && Shape<L>::E == 8;
+  static constexpr bool CAP = L == 9 && THREADS == 128 && Shape<L, MB>::E == 8;
   static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
   static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
 };
@@ -178,9 +188,9 @@ template <typename T, int L, bool WIDE = false>
 __host__ __device__ constexpr size_t col_smem_bytes() {
   return ColCfg<T, L, WIDE>::P_BYTES + ColCfg<T, L, WIDE>::X_BYTES;
 }
-template <typename T, int L>
+template <typename T, int L, int MB = 0>
 __host__ __device__ constexpr size_t row_smem_bytes() {
-  return sizeof(cx<T>) * RowCfg<L>::B * RowCfg<L>::S;
+  return sizeof(cx<T>) * RowCfg<L, MB>::B * RowCfg<L, MB>::S;
 }
 
 // ---------------------------------------------------------------------------
@@ -347,11 +357,13 @@ col_fft_kernel(const ColParams prm) {
 // r2c along n2 (packed: n2 reals -> N = n2/2 complex FFT -> n2/2+1 bins)
 // ---------------------------------------------------------------------------
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::MINB_R2C)
+__global__ void __launch_bounds__(RowCfg<L, r2c_radix_bits(L, sizeof(T))>::THREADS,
+                                  RowCfg<L, r2c_radix_bits(L, sizeof(T))>::MINB_R2C)
 r2c_rows_kernel(const RowParams prm) {
-  using RC = RowCfg<L>;
-  using SH = Shape<L>;
-  using ST = Stockham<T, L, false, RC::S, RC::PS>;
+  constexpr int MB = r2c_radix_bits(L, sizeof(T));
+  using RC = RowCfg<L, MB>;
+  using SH = Shape<L, MB>;
+  using ST = Stockham<T, L, false, RC::S, RC::PS, false, 0, false, MB>;
   constexpr int N = SH::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);

@@ -207,7 +207,8 @@ struct tffft_plan_s {
   bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
   void* tw0 = nullptr;
   void* tw1 = nullptr;
-  void* tw2 = nullptr;
+  void* tw2 = nullptr;   // row pass tables (c2r, fused stage 1)
+  void* tw2r = nullptr;  // row pass tables in the r2c kernel's schedule
   void* tw2post = nullptr;
   unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles)
   double* row_stats = nullptr;          // per row records of the c2r kernel
@@ -238,13 +239,13 @@ static int ilog2(long long n) { int l = 0; while ((1LL << l) < n) ++l; return l;
 
 // pass twiddle tables for length 2^L (see fft_engine.cuh): block for pass p>=1
 // holds exp(-2 pi i k / (Ns R)) at [k], k < Ns
-static std::vector<double> pass_table(int L) {
+static std::vector<double> pass_table(int L, int mb = 0) {
   std::vector<double> t;
-  const int P = num_passes(L);
-  t.assign(2 * (size_t)std::max(tw_total(L), 1), 0.0);
+  const int P = num_passes(L, mb);
+  t.assign(2 * (size_t)std::max(tw_total(L, mb), 1), 0.0);
   for (int p = 1; p < P; ++p) {
-    const long long R = 1LL << pass_bits(L, p), NS = 1LL << ns_bits(L, p), M = NS * R;
-    const size_t off = tw_offset(L, p);
+    const long long R = 1LL << pass_bits(L, p, mb), NS = 1LL << ns_bits(L, p, mb), M = NS * R;
+    const size_t off = tw_offset(L, p, mb);
     for (long long k = 0; k < NS; ++k) {
       const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / (long double)M;
       t[2 * (off + k)] = (double)cosl(a);
@@ -303,8 +304,10 @@ static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd
 }
 static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
-  return pl->dtype == TFFFT_F64 ? launch_r2c_rows<double>(pl->L2h, prm, s)
-                                : launch_r2c_rows<float>(pl->L2h, prm, s);
+  RowParams q = prm;
+  q.tw = pl->tw2r;  // the r2c kernel's own radix schedule (r2c_radix_bits)
+  return pl->dtype == TFFFT_F64 ? launch_r2c_rows<double>(pl->L2h, q, s)
+                                : launch_r2c_rows<float>(pl->L2h, q, s);
 }
 static cudaError_t c2r_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
@@ -956,6 +959,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   TRY(upload_table(pass_table(pl->L0), dtype, &pl->tw0, &ws));
   TRY(upload_table(pass_table(pl->L1), dtype, &pl->tw1, &ws));
   TRY(upload_table(pass_table(pl->L2h), dtype, &pl->tw2, &ws));
+  TRY(upload_table(pass_table(pl->L2h, r2c_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2r, &ws));
   TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
   CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
@@ -1047,7 +1051,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   if (!pl) return TFFFT_OK;
   cudaSetDevice(pl->comm->device);
   free_events(pl);
-  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2post);
+  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2post);
   cudaFree(pl->stats); cudaFree(pl->row_stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
   cudaFree(pl->band_dst);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
