@@ -61,28 +61,67 @@ def algorithmic_bytes(n0, n1, n2, p, s_r):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks, power and clock-event (throttle) reasons sampled during the
+    timed region: NVML in-process every 10 ms (the device matched by PCI bus
+    id), else nvidia-smi every ~0.2 s."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, {reason names}, watts)
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            prop = torch.cuda.get_device_properties(device)  # integer PCI ids
+            want = (prop.pci_domain_id, prop.pci_bus_id, prop.pci_device_id)
+            self._h = None
+            for i in range(nv.nvmlDeviceGetCount()):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                pci = nv.nvmlDeviceGetPciInfo(h)
+                if (pci.domain, pci.bus, pci.device) == want:
+                    self._h = h
+                    break
+            if self._h is None:
+                raise RuntimeError("no NVML device with the CUDA device's PCI id")
+            self._bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                          "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                          "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self._nvml = nv
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml, self._h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        watts = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        return (float(sm), float(mx), {n for n, b in self._bits.items() if bits & b}, watts)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        num = lambda x: float(x) if x.replace(".", "").isdigit() else None
+        return (num(f[0]), num(f[1]), {n for n, v in zip(self.NAMES, f[2:6]) if "Active" in v and "Not" not in v},
+                num(f[6]) if len(f) > 6 else None)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 return
-            self._stop.wait(0.2)
+            self._stop.wait(0.01 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -97,13 +136,14 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return None
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
-                          and "Not" not in s[2 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples if s[0] is not None]
+        mx = [s[1] for s in self.samples if s[1] is not None]
+        w = [s[3] for s in self.samples if s[3] is not None]
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w_median": statistics.median(w) if w else None,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -262,6 +302,8 @@ def run_gpu(args):
         for _ in range(args.steps):
             step()
         e1.record(stream)
+        while not e1.query():  # wait without holding the GIL, so the clock sampler keeps sampling
+            time.sleep(0.002)
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     launches = fp.launches
@@ -356,7 +398,7 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--grid", type=int, default=1024)
