@@ -405,7 +405,7 @@ def main():
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
     ap.add_argument("--config", choices=["cube", "turbulence"], default="cube",
                     help="cube: seeded uniform field pair (headline); turbulence: BASELINE config 5")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-planes", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
