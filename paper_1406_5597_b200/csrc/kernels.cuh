@@ -32,10 +32,12 @@ struct ColParams {
   long long inner_stride, block_stride;
   int band_shift, self_band;
   long long stg_band, stg_within, stg_grp;
+  long long stg_base;     // added to every staging / landing offset (plane chunk of stage 1b)
   // L2 prefetch of wide row segments for the tile `pf_ahead` tiles ahead
   // (0 = off): DRAM then sees pf_bytes-wide row visits instead of B*sizeof(cx)
   long long pf_ahead;
   int pf_bytes;
+  int probe;  // profiling probes (0 = off): bit 0 skips the epilogue stores, bit 1 the prefetch loads
 };
 
 // Rows: row r of real data at real + r*n2 (reals); complex row at spec + r*n2c.
@@ -93,11 +95,18 @@ struct RowParams {
 // shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
 // WIDE (stage 3, rows megabytes apart): 128-byte row visits, i.e. 8 float64 or
 // 16 float32 columns; otherwise 8 columns
+#ifndef TFFFT_COL_SMEM_KB
+#define TFFFT_COL_SMEM_KB 227
+#endif
+#ifndef TFFFT_COL_MINTHREADS
+#define TFFFT_COL_MINTHREADS 256
+#endif
 template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
   constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_NARROW_B;
-  int b = 256 / TPT > want ? 256 / TPT : want;
+  constexpr int mt = L == 10 && sizeof(T) == 8 ? TFFFT_COL_MINTHREADS : 256;
+  int b = mt / TPT > want ? mt / TPT : want;
   // split exchange: prefetch slots (complex) + exchange buffer (real words);
   // whole-complex exchange: the next tile's operands fit slots + exchange buffer
   constexpr size_t per_elem = TFFFT_SPLIT ? sizeof(cx<T>) + sizeof(T) : sizeof(cx<T>);
@@ -135,7 +144,7 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
   // while the tile computes; when slots for all E do not fit beside the
   // exchange buffer, the other LO_E are fetched into the exchange buffer as
   // soon as the tile's last exchange has drained it.
-  static constexpr size_t SMEM_MAX = 227 * 1024;
+  static constexpr size_t SMEM_MAX = (size_t)(L == 10 && sizeof(T) == 8 && THREADS <= 128 ? TFFFT_COL_SMEM_KB : 227) * 1024;
   static constexpr int PF_FIT = (int)((SMEM_MAX - X_BYTES) / (sizeof(cx<T>) * THREADS));
   static constexpr int PF_E = !PREFETCH ? 0 : (PF_FIT < Shape<L>::E ? PF_FIT : Shape<L>::E);
   static constexpr int LO_E = PREFETCH ? Shape<L>::E - PF_E : 0;
@@ -254,18 +263,20 @@ col_fft_kernel(const ColParams prm) {
     if constexpr (RD == 2) {
       const int band = (int)(e >> prm.band_shift);
       if (band != prm.self_band)
-        return reinterpret_cast<const cx<T>*>(prm.staging) + ((long long)col.cq * prm.stg_grp + col.cr) +
+        return reinterpret_cast<const cx<T>*>(prm.staging) + ((long long)col.cq * prm.stg_grp + col.cr + prm.stg_base) +
                (long long)band * prm.stg_band + (long long)(e & bmask) * prm.stg_within;
     }
     return col.p + offset(e);
   };
   cx<T>* lo = reinterpret_cast<cx<T>*>(xs);  // [LO_E][NT] leftover slots inside the exchange buffer
   auto prefetch = [&](const Col& col) {
+    if (prm.probe & 2) return;
 #pragma unroll
     for (int kk = 0; kk < CF::PF_E; ++kk) cp_async<sizeof(cx<T>)>(pf + kk * NT + t, src(col, tt + TPT * kk));
     cp_commit();
   };
   auto prefetch_lo = [&](const Col& col) {
+    if (prm.probe & 2) return;
 #pragma unroll
     for (int kk = CF::PF_E; kk < E; ++kk)
       cp_async<sizeof(cx<T>)>(lo + (kk - CF::PF_E) * NT + t, src(col, tt + TPT * kk));
@@ -275,6 +286,10 @@ col_fft_kernel(const ColParams prm) {
   long long tile = blockIdx.x / CL;
   const long long tstep = gridDim.x / CL;
   if (tile >= ntiles) return;
+  if ((prm.probe >> 8) && (blockIdx.x & 1)) {  // probe: desynchronise odd CTAs by probe>>8 ns
+    const unsigned d = (unsigned)(prm.probe >> 8);
+    for (unsigned w = 0; w < d; w += 1000) __nanosleep(1000);
+  }
   Col cur = column(tile);
   if (CF::PREFETCH) prefetch(cur);
   if (CF::LO_E > 0) prefetch_lo(cur);
@@ -324,9 +339,9 @@ col_fft_kernel(const ColParams prm) {
       ST::finish(xs, v, tt, bl, tw);
     }
 
-    if (cur.valid) {
+    if (cur.valid && !(prm.probe & 1)) {
       if constexpr (RD == 1) {
-        const long long cofs = (long long)cur.cq * prm.stg_grp + cur.cr;
+        const long long cofs = (long long)cur.cq * prm.stg_grp + cur.cr + prm.stg_base;
         const unsigned sw = (unsigned)prm.stg_within;
 #pragma unroll
         for (int u = 0; u < E / SH::RL; ++u)

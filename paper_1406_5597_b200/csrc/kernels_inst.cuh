@@ -6,6 +6,7 @@
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
+#include "col_ws.cuh"
 
 namespace tffft {
 
@@ -236,6 +237,33 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
   switch (L) {
     case 10: return inv ? ft_one<TFFFT_REAL, 5, 5, true>(maps, p, s) : ft_one<TFFFT_REAL, 5, 5, false>(maps, p, s);
     case 12: return inv ? ft_one<TFFFT_REAL, 6, 6, true>(maps, p, s) : ft_one<TFFFT_REAL, 6, 6, false>(maps, p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int L, bool INV>
+static cudaError_t ws_one(const CUtensorMap& map, const WsParams& p, cudaStream_t s) {
+  using CF = WsCfg<T, L>;
+  auto k = col_ws_kernel<T, L, INV>;
+  static cudaError_t prep = prep_smem(k, CF::SMEM);
+  if (prep != cudaSuccess) return prep;
+  if (p.ntiles <= 0) return cudaSuccess;
+  static int per_sm = [&] {
+    int n = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CF::THREADS, CF::SMEM);
+    return n < 1 ? 1 : n;
+  }();
+  const long long blocks = std::min<long long>(p.ntiles, (long long)per_sm * num_sms());
+  (void)cudaGetLastError();
+  k<<<(unsigned)blocks, CF::THREADS, CF::SMEM, s>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_col_ws<TFFFT_REAL>(int L, bool inv, const CUtensorMap& map, const WsParams& p, cudaStream_t s) {
+  switch (L) {
+    case 9: return inv ? ws_one<TFFFT_REAL, 9, true>(map, p, s) : ws_one<TFFFT_REAL, 9, false>(map, p, s);
+    case 10: return inv ? ws_one<TFFFT_REAL, 10, true>(map, p, s) : ws_one<TFFFT_REAL, 10, false>(map, p, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -29,6 +29,7 @@
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
+#include "col_ws.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 
@@ -225,6 +226,12 @@ struct tffft_plan_s {
   // fused stage 1 (stage1_fused.cuh)
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
+  // stage 1 pipelined over plane chunks on two streams (row kernel on s1_aux,
+  // column kernel on the caller's stream): a chunk's intermediate stays in L2
+  int s1_chunk = 0;      // planes per chunk (0 = whole slab, one launch per kernel)
+  int s1_depth = 2;      // row chunks in flight ahead of the column kernel
+  cudaStream_t s1_aux = nullptr;
+  std::vector<cudaEvent_t> s1_ev_row, s1_ev_col;
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -296,9 +303,14 @@ static int upload_table(const std::vector<double>& t, int dtype, void** dev, siz
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 // ---------------------------------------------------------------------------
-static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd, bool wide, const ColParams& prm,
+static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd, bool wide, const ColParams& prm0,
                               cudaStream_t s) {
   pl->launches++;
+  ColParams prm = prm0;
+  {
+    static const char* probe = getenv("TFFFT_PROBE_COL");
+    prm.probe = probe ? atoi(probe) : 0;
+  }
   return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, two, rd, wide, prm, s)
                                 : launch_col_fft<float>(L, inv, two, rd, wide, prm, s);
 }
@@ -357,12 +369,16 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 // ---------------------------------------------------------------------------
 // stage launchers
 // ---------------------------------------------------------------------------
+static int columns_ws(tffft_plan_t pl, int L, bool inv, void* base, long long cols, long long ngrp,
+                      long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
+
 // stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of the local slab
-static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int plane0 = 0, int nplanes = -1) {
+  if (nplanes < 0) nplanes = pl->n0p;
   ColParams c{};
-  c.data = spec;
+  c.data = static_cast<char*>(spec) + (size_t)plane0 * pl->n1 * pl->n2c * pl->esz;
   c.tw = pl->tw1;
-  c.ncols = (long long)pl->n0p * pl->n2c;
+  c.ncols = (long long)nplanes * pl->n2c;
   c.cpb = pl->n2c;
   c.grp_stride = (long long)pl->n1 * pl->n2c;
   c.ic_shift = 30;
@@ -381,6 +397,17 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
+    c.stg_base = (long long)plane0 * c.stg_grp;
+  }
+  {  // profiling probe: every plane aliases plane 0 (same work, L2-resident footprint)
+    static const char* probe = getenv("TFFFT_PROBE_ALIAS");
+    if (probe && atoi(probe)) c.grp_stride = 0;
+  }
+  if (rd == 0 && c.grp_stride != 0) {
+    bool done = false;
+    TRY(columns_ws(pl, pl->L1, inv, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c, pl->tw1, s,
+                   &done));
+    if (done) return TFFFT_OK;
   }
   CUDA_TRY(col_launch(pl, pl->L1, inv, false, rd, false, c, s));
   return TFFFT_OK;
@@ -404,15 +431,66 @@ static EncodeTiledFn encode_tiled() {
 
 // rank-r map over `base` in real elements of the plan's precision; dims/strides innermost first
 static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const cuuint64_t* dims,
-                    const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+                    const cuuint64_t* strides_bytes, const cuuint32_t* box,
+                    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = fn(m, pl->dtype == TFFFT_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         (cuuint32_t)rank, base, dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TFFFT_OK;
+}
+
+// Column pass through the warp-specialised TMA kernel (col_ws.cuh): `ngrp`
+// groups of `cols` contiguous columns, column elements `rstride` apart, groups
+// `gstride` apart (elements).  Returns TFFFT_OK with *done = false when the
+// shape is not supported (the caller falls back to col_fft_kernel).
+static bool ws_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TFFFT_WS");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return on;
+}
+static int columns_ws(tffft_plan_t pl, int L, bool inv, void* base, long long cols, long long ngrp,
+                      long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
+  *done = false;
+  const long long esz = (long long)pl->esz, W = 64 / esz;
+  if (!ws_enabled() || !col_ws_supported(L) || (rstride * esz) % 16 || (gstride * esz) % 16 ||
+      reinterpret_cast<uintptr_t>(base) % 16)
+    return TFFFT_OK;
+  CUtensorMap map;
+  const long long n = 1LL << L;
+  cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
+  cuuint64_t st[2] = {(cuuint64_t)(rstride * esz), (cuuint64_t)(ngrp > 1 ? gstride * esz : n * rstride * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)std::min<long long>(n, 256), 1};
+  static const int promo = [] {
+    const char* e = getenv("TFFFT_WS_PROMO");
+    return e ? atoi(e) : 0;
+  }();
+  static const CUtensorMapL2promotion promos[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+  TRY(make_map(pl, &map, base, 3, d, st, box, promos[promo & 3]));
+  WsParams w{};
+  {
+    static const char* ef = getenv("TFFFT_WS_EF");
+    w.evict_first = ef ? atoi(ef) : 1;
+  }
+  w.data = base;
+  w.tw = tw;
+  w.tpg = (int)((cols + W - 1) / W);
+  w.ntiles = (long long)w.tpg * ngrp;
+  w.cols = (int)cols;
+  w.rstride = rstride;
+  w.gstride = gstride;
+  pl->launches++;
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_ws<double>(L, inv, map, w, s)
+                                               : launch_col_ws<float>(L, inv, map, w, s);
+  CUDA_TRY(e);
+  *done = true;
   return TFFFT_OK;
 }
 
@@ -493,6 +571,12 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     CUDA_TRY(fs_launch(pl, inv, pl->p == 1 ? 0 : (f.staging ? 3 : 2), f, s));
     return TFFFT_OK;
   }
+  if (pl->p == 1) {
+    bool done = false;
+    TRY(columns_ws(pl, pl->L0, inv, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0, pl->tw0, s,
+                   &done));
+    if (done) return TFFFT_OK;
+  }
   ColParams c{};
   c.data = spec;
   c.tw = pl->tw0;
@@ -531,18 +615,52 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   return TFFFT_OK;
 }
 
-static RowParams row_params(tffft_plan_t pl, void* real, void* spec) {
+static RowParams row_params(tffft_plan_t pl, void* real, void* spec, int plane0 = 0, int nplanes = -1) {
+  if (nplanes < 0) nplanes = pl->n0p;
+  const long long row0 = (long long)plane0 * pl->n1;
   RowParams r{};
-  r.real = real;
-  r.spec = spec;
+  r.real = static_cast<char*>(real) + (size_t)row0 * pl->n2 * (pl->esz / 2);
+  r.spec = static_cast<char*>(spec) + (size_t)row0 * pl->n2c * pl->esz;
   r.tw = pl->tw2;
   r.tw_post = pl->tw2post;
-  r.nrows = (long long)pl->n0p * pl->n1;
+  r.nrows = (long long)nplanes * pl->n1;
   r.n2c = pl->n2c;
   r.rows_per_plane = pl->n1;
   r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
-  r.row_stats = pl->row_stats;
+  r.row_stats = pl->row_stats + 3 * row0;
   return r;
+}
+
+// Stage 1 / 1' over plane chunks of pl->s1_chunk planes, two streams:
+//   forward : aux  r2c(c) -> ev_row[c]          main: wait ev_row[c], columns(c) -> ev_col[c]
+//   inverse : main columns'(c) -> ev_col[c]      aux : wait ev_col[c], c2r(c) -> ev_row[c]
+// The producer of chunk c + depth waits for the consumer of chunk c, so at most
+// depth + 1 chunks of intermediate planes are live: they stay in L2 between the
+// row and column kernels, and the two kernels fill each other's tails.
+static int stage1_pipelined(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaStream_t s) {
+  const int K = pl->s1_chunk, nch = (pl->n0p + K - 1) / K, D = pl->s1_depth;
+  const int R = (int)pl->s1_ev_row.size();
+  cudaStream_t a = pl->s1_aux;
+  cudaStream_t prod = fwd ? a : s, cons = fwd ? s : a;
+  CUDA_TRY(cudaEventRecord(pl->s1_ev_col[R - 1], s));  // fork: aux ordered after everything before
+  CUDA_TRY(cudaStreamWaitEvent(a, pl->s1_ev_col[R - 1], 0));
+  for (int c = 0; c < nch; ++c) {
+    const int p0 = c * K, np = std::min(K, pl->n0p - p0);
+    cudaEvent_t evp = pl->s1_ev_row[c % (R - 1)], evc = pl->s1_ev_col[c % (R - 1)];
+    if (c >= D) CUDA_TRY(cudaStreamWaitEvent(prod, pl->s1_ev_col[(c - D) % (R - 1)], 0));
+    if (fwd) CUDA_TRY(r2c_launch(pl, row_params(pl, real, spec, p0, np), prod));
+    else TRY(stage1_columns(pl, spec, true, prod, p0, np));
+    CUDA_TRY(cudaEventRecord(evp, prod));
+    CUDA_TRY(cudaStreamWaitEvent(cons, evp, 0));
+    if (fwd) TRY(stage1_columns(pl, spec, false, cons, p0, np));
+    else CUDA_TRY(c2r_launch(pl, row_params(pl, real, spec, p0, np), cons));
+    CUDA_TRY(cudaEventRecord(evc, cons));
+  }
+  if (!fwd) {  // join: the caller's stream continues after the last c2r
+    CUDA_TRY(cudaEventRecord(pl->s1_ev_row[R - 1], a));
+    CUDA_TRY(cudaStreamWaitEvent(s, pl->s1_ev_row[R - 1], 0));
+  }
+  return TFFFT_OK;
 }
 
 // fused stage 1 / 1': one persistent kernel per direction, planes stay in L2
@@ -797,6 +915,12 @@ static int unpack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
 
 // stage 3 / 3' over the CONTIGUOUS_FLIPPED layout: column (j, k) at stride n2c
 static int stage3_flipped(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
+  if (pl->p == 1) {
+    bool done = false;
+    TRY(columns_ws(pl, pl->L0, inv, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0, pl->tw0, s,
+                   &done));
+    if (done) return TFFFT_OK;
+  }
   ColParams c{};
   c.data = spec;
   c.tw = pl->tw0;
@@ -1023,6 +1147,23 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
     }
   }
+  {
+    static const char* env_k = getenv("TFFFT_S1_CHUNK");
+    static const char* env_d = getenv("TFFFT_S1_DEPTH");
+    const int K = env_k ? atoi(env_k) : 0;
+    if (K > 0 && !pl->s1_fused && strategy == 0 && K < pl->n0p) {
+      pl->s1_chunk = K;
+      pl->s1_depth = env_d ? std::max(1, atoi(env_d)) : 2;
+      CUDA_TRY(cudaStreamCreateWithFlags(&pl->s1_aux, cudaStreamNonBlocking));
+      const int R = pl->s1_depth + 2;
+      pl->s1_ev_row.resize(R);
+      pl->s1_ev_col.resize(R);
+      for (int i = 0; i < R; ++i) {
+        CUDA_TRY(cudaEventCreateWithFlags(&pl->s1_ev_row[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&pl->s1_ev_col[i], cudaEventDisableTiming));
+      }
+    }
+  }
   pl->workspace = ws;
   *out = pl.release();
   return TFFFT_OK;
@@ -1057,6 +1198,9 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
+  for (auto e : pl->s1_ev_row) cudaEventDestroy(e);
+  for (auto e : pl->s1_ev_col) cudaEventDestroy(e);
+  if (pl->s1_aux) cudaStreamDestroy(pl->s1_aux);
   delete pl;
   return TFFFT_OK;
 }
@@ -1095,6 +1239,8 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
   TRY(fabric_guard_staging(pl, s));
   if (pl->s1_fused) {
     TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
+  } else if (pl->s1_chunk > 0) {
+    TRY(stage1_pipelined(pl, const_cast<void*>(real_in), spec_out, true, s));
   } else {
     CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
     TRY(stage1_columns(pl, spec_out, false, s));
@@ -1150,6 +1296,9 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   // stage 1' (dfft.py:206-209)
   if (pl->s1_fused) {
     TRY(stage1_fused(pl, real_out, spec, false, s));
+  } else if (pl->s1_chunk > 0) {
+    TRY(stage1_pipelined(pl, real_out, spec, false, s));
+    TRY(fabric_landing_consumed(pl, s));
   } else {
     TRY(stage1_columns(pl, spec, true, s));
     TRY(fabric_landing_consumed(pl, s));
