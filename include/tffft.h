@@ -85,9 +85,12 @@ enum {
   TFFFT_FLAG_TRANSPOSE = 4,       /* Strategy.TRANSPOSE (exchange.py:195-260): pack, contiguous exchange,
                                      unpack; the spectrum comes out CONTIGUOUS_FLIPPED, element (j, r, k)
                                      at j*n0*n2c + r*n2c + k (layout.py:42-44) -- the paper's baseline */
-  TFFFT_FLAG_PEER_STORES = 8      /* fused exchange: the stage-1 / stage-3' epilogues store every peer band
+  TFFFT_FLAG_PEER_STORES = 8,     /* fused exchange: the stage-1 / stage-3' epilogues store every peer band
                                      straight into the peer's landing buffer (peer memory), and the
                                      exchange reduces to a barrier.  Local fabric communicators. */
+  TFFFT_FLAG_TMA_COLUMNS = 16     /* p = 1 column passes of length 512 / 1024 fed by TMA box copies
+                                     (col_ws.cuh) wherever the row stride allows; without flags
+                                     (flags < 0) only the measured winner, float32 stage 3, uses them */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

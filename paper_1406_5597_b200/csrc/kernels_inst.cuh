@@ -241,30 +241,41 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
   }
 }
 
-template <typename T, int L, bool INV>
-static cudaError_t ws_one(const CUtensorMap& map, const WsParams& p, cudaStream_t s) {
-  using CF = WsCfg<T, L>;
-  auto k = col_ws_kernel<T, L, INV>;
-  static cudaError_t prep = prep_smem(k, CF::SMEM);
+template <typename T, int L, bool INV, bool WIDE>
+static cudaError_t tc_one(const CUtensorMap& map, const TmaColParams& p, cudaStream_t s) {
+  using TC = TmaColCfg<T, L, WIDE>;
+  auto k = col_tma_kernel<T, L, INV, WIDE>;
+  static cudaError_t prep = prep_smem(k, TC::SMEM);
   if (prep != cudaSuccess) return prep;
   if (p.ntiles <= 0) return cudaSuccess;
-  static int per_sm = [&] {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CF::THREADS, CF::SMEM);
-    return n < 1 ? 1 : n;
-  }();
-  const long long blocks = std::min<long long>(p.ntiles, (long long)per_sm * num_sms());
+  const long long blocks = std::min<long long>(p.ntiles, num_sms());
   (void)cudaGetLastError();
-  k<<<(unsigned)blocks, CF::THREADS, CF::SMEM, s>>>(map, p);
+  k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, p);
   return cudaGetLastError();
 }
 
+template <typename T, int L>
+static cudaError_t tc_dispatch(bool inv, bool wide, const CUtensorMap& map, const TmaColParams& p, cudaStream_t s) {
+  if (wide) return inv ? tc_one<T, L, true, true>(map, p, s) : tc_one<T, L, false, true>(map, p, s);
+  return inv ? tc_one<T, L, true, false>(map, p, s) : tc_one<T, L, false, false>(map, p, s);
+}
+
 template <>
-cudaError_t launch_col_ws<TFFFT_REAL>(int L, bool inv, const CUtensorMap& map, const WsParams& p, cudaStream_t s) {
+cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, const CUtensorMap& map, const TmaColParams& p,
+                                       cudaStream_t s) {
   switch (L) {
-    case 9: return inv ? ws_one<TFFFT_REAL, 9, true>(map, p, s) : ws_one<TFFFT_REAL, 9, false>(map, p, s);
-    case 10: return inv ? ws_one<TFFFT_REAL, 10, true>(map, p, s) : ws_one<TFFFT_REAL, 10, false>(map, p, s);
+    case 9: return tc_dispatch<TFFFT_REAL, 9>(inv, wide, map, p, s);
+    case 10: return tc_dispatch<TFFFT_REAL, 10>(inv, wide, map, p, s);
     default: return cudaErrorInvalidValue;
+  }
+}
+
+template <>
+int col_tma_width<TFFFT_REAL>(int L, bool wide) {
+  switch (L) {
+    case 9: return wide ? TmaColCfg<TFFFT_REAL, 9, true>::B : TmaColCfg<TFFFT_REAL, 9, false>::B;
+    case 10: return wide ? TmaColCfg<TFFFT_REAL, 10, true>::B : TmaColCfg<TFFFT_REAL, 10, false>::B;
+    default: return 0;
   }
 }
 

@@ -226,6 +226,7 @@ struct tffft_plan_s {
   // fused stage 1 (stage1_fused.cuh)
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
+  int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 stage 3 only
   // stage 1 pipelined over plane chunks on two streams (row kernel on s1_aux,
   // column kernel on the caller's stream): a chunk's intermediate stays in L2
   int s1_chunk = 0;      // planes per chunk (0 = whole slab, one launch per kernel)
@@ -369,8 +370,8 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 // ---------------------------------------------------------------------------
 // stage launchers
 // ---------------------------------------------------------------------------
-static int columns_ws(tffft_plan_t pl, int L, bool inv, void* base, long long cols, long long ngrp,
-                      long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
+static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
+                       long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
 // stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of the local slab
 static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int plane0 = 0, int nplanes = -1) {
@@ -405,8 +406,8 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
   }
   if (rd == 0 && c.grp_stride != 0) {
     bool done = false;
-    TRY(columns_ws(pl, pl->L1, inv, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c, pl->tw1, s,
-                   &done));
+    TRY(columns_tma(pl, pl->L1, inv, false, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
+                    pl->tw1, s, &done));
     if (done) return TFFFT_OK;
   }
   CUDA_TRY(col_launch(pl, pl->L1, inv, false, rd, false, c, s));
@@ -444,51 +445,43 @@ static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const
   return TFFFT_OK;
 }
 
-// Column pass through the warp-specialised TMA kernel (col_ws.cuh): `ngrp`
-// groups of `cols` contiguous columns, column elements `rstride` apart, groups
-// `gstride` apart (elements).  Returns TFFFT_OK with *done = false when the
-// shape is not supported (the caller falls back to col_fft_kernel).
-static bool ws_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("TFFFT_WS");
-    return e ? atoi(e) != 0 : false;
-  }();
-  return on;
+// Column pass through the TMA-fed column kernel (col_ws.cuh): `ngrp` groups
+// of `cols` contiguous columns, column elements `rstride` apart, groups
+// `gstride` apart (elements).  Sets *done = false when the shape has no TMA
+// path (the caller falls back to col_fft_kernel).
+static bool tma_cols_enabled(tffft_plan_t pl, bool wide) {
+  return pl->tma_cols == 1 || (pl->tma_cols == 2 && wide && pl->dtype == TFFFT_F32);
 }
-static int columns_ws(tffft_plan_t pl, int L, bool inv, void* base, long long cols, long long ngrp,
-                      long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
+static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
+                       long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
   *done = false;
-  const long long esz = (long long)pl->esz, W = 64 / esz;
-  if (!ws_enabled() || !col_ws_supported(L) || (rstride * esz) % 16 || (gstride * esz) % 16 ||
+  const long long esz = (long long)pl->esz;
+  if (!tma_cols_enabled(pl, wide) || !col_tma_supported(L) || (rstride * esz) % 16 || (ngrp > 1 && (gstride * esz) % 16) ||
       reinterpret_cast<uintptr_t>(base) % 16)
     return TFFFT_OK;
+  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
+  if (B <= 0) return TFFFT_OK;
   CUtensorMap map;
   const long long n = 1LL << L;
   cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
   cuuint64_t st[2] = {(cuuint64_t)(rstride * esz), (cuuint64_t)(ngrp > 1 ? gstride * esz : n * rstride * esz)};
-  cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)std::min<long long>(n, 256), 1};
-  static const int promo = [] {
-    const char* e = getenv("TFFFT_WS_PROMO");
-    return e ? atoi(e) : 0;
-  }();
-  static const CUtensorMapL2promotion promos[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
-                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
-  TRY(make_map(pl, &map, base, 3, d, st, box, promos[promo & 3]));
-  WsParams w{};
-  {
-    static const char* ef = getenv("TFFFT_WS_EF");
-    w.evict_first = ef ? atoi(ef) : 1;
-  }
+  cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n, 256), 1};
+  TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+  TmaColParams w{};
   w.data = base;
   w.tw = tw;
-  w.tpg = (int)((cols + W - 1) / W);
+  w.tpg = (int)((cols + B - 1) / B);
   w.ntiles = (long long)w.tpg * ngrp;
   w.cols = (int)cols;
   w.rstride = rstride;
   w.gstride = gstride;
+  {
+    static const char* ef = getenv("TFFFT_TMA_EF");
+    w.evict_first = ef ? atoi(ef) : ((rstride * esz) % 128 == 0);
+  }
   pl->launches++;
-  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_ws<double>(L, inv, map, w, s)
-                                               : launch_col_ws<float>(L, inv, map, w, s);
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, map, w, s)
+                                               : launch_col_tma<float>(L, inv, wide, map, w, s);
   CUDA_TRY(e);
   *done = true;
   return TFFFT_OK;
@@ -573,8 +566,8 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   }
   if (pl->p == 1) {
     bool done = false;
-    TRY(columns_ws(pl, pl->L0, inv, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0, pl->tw0, s,
-                   &done));
+    TRY(columns_tma(pl, pl->L0, inv, true, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0,
+                    pl->tw0, s, &done));
     if (done) return TFFFT_OK;
   }
   ColParams c{};
@@ -917,8 +910,8 @@ static int unpack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
 static int stage3_flipped(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s) {
   if (pl->p == 1) {
     bool done = false;
-    TRY(columns_ws(pl, pl->L0, inv, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0, pl->tw0, s,
-                   &done));
+    TRY(columns_tma(pl, pl->L0, inv, true, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0,
+                    pl->tw0, s, &done));
     if (done) return TFFFT_OK;
   }
   ColParams c{};
@@ -1027,6 +1020,8 @@ int tffft_comm_destroy(tffft_comm_t c) {
 
 static int env_flags() {
   int f = 0;
+  const char* tc = getenv("TFFFT_TMA_COLS");
+  if (tc && atoi(tc) != 0) f |= TFFFT_FLAG_TMA_COLUMNS;
   const char* fuse = getenv("TFFFT_FUSE");
   const char* fs = getenv("TFFFT_FOURSTEP");
   if (fuse && atoi(fuse) != 0) f |= TFFFT_FLAG_FUSED_STAGE1;
@@ -1041,13 +1036,24 @@ int tffft_plan_create(int n0, int n1, int n2, int dtype, int pattern, tffft_comm
 int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   if (!pl || !flags) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0) |
-           (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0) | (pl->peer_stores ? TFFFT_FLAG_PEER_STORES : 0);
+           (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0) | (pl->peer_stores ? TFFFT_FLAG_PEER_STORES : 0) |
+           (pl->tma_cols == 1 ? TFFFT_FLAG_TMA_COLUMNS : 0);
   return TFFFT_OK;
 }
 
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* out) {
-  if (flags < 0) flags = env_flags();
+  // TMA column passes: explicit flag = every supported pass; environment
+  // defaults = the measured winner (float32 stage 3, profiles/r01s2/tma_cols.txt)
+  // unless TFFFT_TMA_COLS says otherwise
+  int tma_cols = 0;
+  if (flags < 0) {
+    flags = env_flags();
+    const char* tc = getenv("TFFFT_TMA_COLS");
+    tma_cols = (flags & TFFFT_FLAG_TMA_COLUMNS) ? 1 : (tc ? 0 : 2);
+  } else {
+    tma_cols = (flags & TFFFT_FLAG_TMA_COLUMNS) ? 1 : 0;
+  }
   if (!comm || !out) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   const int p = comm->p;
   // layout.py:63-66 (powers of two), layout.py:83-93 (validate)
@@ -1077,6 +1083,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   pl->n0p = n0 / p; pl->n1p = n1 / p; pl->n2c = n2 / 2 + 1;
   pl->esz = dtype == TFFFT_F64 ? 16 : 8;
   pl->strategy = strategy;
+  pl->tma_cols = (p == 1 && strategy == 0) ? tma_cols : 0;
   CUDA_TRY(cudaSetDevice(comm->device));
 
   size_t ws = 0;

@@ -115,7 +115,7 @@ class FftPlan:
             pass
 
 
-ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8}
+ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8, "tma_columns": 16}
 TRANSPOSE_FLAG = 4
 
 
@@ -132,8 +132,9 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric.
 
     ``algorithms`` selects optional kernel schedules ("fused_stage1",
-    "fourstep_stage3"); None takes the library defaults (TFFFT_FUSE /
-    TFFFT_FOURSTEP environment switches)."""
+    "fourstep_stage3", "peer_stores", "tma_columns"); None takes the library
+    defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS environment
+    switches; by default float32 stage 3 at p = 1 is TMA-fed)."""
     validate(grid, comm.p)
     if not isinstance(comm_pattern, CommPattern):
         raise ConfigurationError(f"comm_pattern must be a CommPattern, got {comm_pattern!r}")

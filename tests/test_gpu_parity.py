@@ -379,3 +379,44 @@ def test_collective_pattern_matches_pairwise(shape, p, strategy):
         assert a[2] == b[2]
         assert rel(b[0].reshape(-1), want[:, q * n1p:(q + 1) * n1p].transpose(1, 0, 2).reshape(-1)) <= 1e-12
         assert rel(b[1], x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL["float64"]
+
+
+TMA_CASES = [((512, 8, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((512, 512, 6), 1), ((64, 512, 32), 2)]
+
+
+@pytest.mark.parametrize("shape,p", TMA_CASES, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_tma_column_kernel_bitwise(shape, p, dtype):
+    """TMA-fed column passes (col_ws.cuh, lengths 512 / 1024, p = 1): the same
+    Stockham arithmetic as the cp.async kernel, so spectra and inverse outputs
+    are bitwise identical to the default kernels, and within tolerance of the
+    oracle.  Covers partial tiles (columns not a multiple of the box width),
+    float32 stage 1b (row stride not 16-byte aligned: falls back) and p = 2
+    (the flag is dropped: the TMA path is single-rank)."""
+    x = oracle.uniform_field(shape, seed=31)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        ref = tf.plan(grid, ep, dtype=dtype, algorithms=())
+        fp = tf.plan(grid, ep, dtype=dtype, algorithms=("tma_columns",))
+        assert fp.algorithms == (("tma_columns",) if p == 1 else ())
+        want = tf.forward(ref, slabs[ep.rank]).data.clone()
+        want_back = tf.inverse(ref, tf.SpectralSlab(ref.spectral_layout, tf.SpectralTag.STRIDED_INPLACE,
+                                                      want.clone())).data.clone()
+        got = tf.forward(fp, slabs[ep.rank]).data.clone()
+        back = tf.inverse(fp, tf.SpectralSlab(fp.spectral_layout, tf.SpectralTag.STRIDED_INPLACE,
+                                              got.clone())).data.clone()
+        return (want.cpu().numpy(), want_back.cpu().numpy(), got.cpu().numpy(), back.cpu().numpy())
+
+    res = tf.run_spmd(p, body)
+    ref = oracle.forward_all(x, p)
+    n0p = shape[0] // p
+    for q in range(p):
+        want, want_back, got, back = res[q]
+        assert np.array_equal(got, want)
+        assert np.array_equal(back, want_back)
+        assert rel(got, ref[q]) <= TOL[dtype]
+        assert rel(back, x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
