@@ -75,6 +75,9 @@ struct RowParams {
 #ifndef TFFFT_NARROW_B
 #define TFFFT_NARROW_B 8
 #endif
+#ifndef TFFFT_NARROW_WIDEN
+#define TFFFT_NARROW_WIDEN 0
+#endif
 #ifndef TFFFT_NARROW_PREFETCH
 #define TFFFT_NARROW_PREFETCH 1
 #endif
@@ -104,7 +107,8 @@ struct RowParams {
 template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
-  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_NARROW_B;
+  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>))
+                            : TFFFT_NARROW_B * (TFFFT_NARROW_WIDEN ? (int)(16 / sizeof(cx<T>)) : 1);
   constexpr int mt = L == 10 && sizeof(T) == 8 ? TFFFT_COL_MINTHREADS : 256;
   int b = mt / TPT > want ? mt / TPT : want;
   // split exchange: prefetch slots (complex) + exchange buffer (real words);
@@ -460,9 +464,15 @@ c2r_rows_kernel(const RowParams prm) {
   constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
   constexpr int SEGS = SH::TPT / W;  // warp segments per row
   __shared__ int seg_m2[RC::B][SEGS];
+  // float32: max(|Re X|, |Im X|) compared as the (non-negative) float's bit
+  // pattern, no conversion to double per element; the record 2 m^2 bounds
+  // max |X|^2 from above (within 2x), well inside the float32 tolerance.
   int m2h = 0;
   double e0 = 0.0, eN = 0.0;
-  auto m2hi = [](cx<T> X) { return __double2hiint(fma((double)X.x, (double)X.x, (double)X.y * X.y)); };
+  auto m2hi = [](cx<T> X) {
+    if constexpr (sizeof(T) == 4) return __float_as_int(fmaxf(fabsf(X.x), fabsf(X.y)));
+    else return __double2hiint(fma((double)X.x, (double)X.x, (double)X.y * X.y));
+  };
 #pragma unroll
   for (int q = 0; q < SH::E; ++q) {
     const int k = tt + SH::TPT * q;
@@ -489,7 +499,12 @@ c2r_rows_kernel(const RowParams prm) {
 #pragma unroll
     for (int g = 1; g < SEGS; ++g) m2h = max(m2h, seg_m2[b][g]);
     double* rec = prm.row_stats + 3 * row;
-    rec[0] = __hiloint2double(m2h, -1);
+    if constexpr (sizeof(T) == 4) {
+      const double m = (double)__int_as_float(m2h);
+      rec[0] = 2.0 * m * m;
+    } else {
+      rec[0] = __hiloint2double(m2h, -1);
+    }
     rec[1] = fmax(e0, eN);
     rec[2] = e0 + eN;
   }
