@@ -75,9 +75,6 @@ struct RowParams {
 #ifndef TFFFT_NARROW_B
 #define TFFFT_NARROW_B 8
 #endif
-#ifndef TFFFT_NARROW_WIDEN
-#define TFFFT_NARROW_WIDEN 0
-#endif
 #ifndef TFFFT_NARROW_PREFETCH
 #define TFFFT_NARROW_PREFETCH 1
 #endif
@@ -98,19 +95,11 @@ struct RowParams {
 // shared memory (prefetch slots B*N complex + ~B*N words of exchange buffer)
 // WIDE (stage 3, rows megabytes apart): 128-byte row visits, i.e. 8 float64 or
 // 16 float32 columns; otherwise 8 columns
-#ifndef TFFFT_COL_SMEM_KB
-#define TFFFT_COL_SMEM_KB 227
-#endif
-#ifndef TFFFT_COL_MINTHREADS
-#define TFFFT_COL_MINTHREADS 256
-#endif
 template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
-  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>))
-                            : TFFFT_NARROW_B * (TFFFT_NARROW_WIDEN ? (int)(16 / sizeof(cx<T>)) : 1);
-  constexpr int mt = L == 10 && sizeof(T) == 8 ? TFFFT_COL_MINTHREADS : 256;
-  int b = mt / TPT > want ? mt / TPT : want;
+  constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_NARROW_B;
+  int b = 256 / TPT > want ? 256 / TPT : want;
   // split exchange: prefetch slots (complex) + exchange buffer (real words);
   // whole-complex exchange: the next tile's operands fit slots + exchange buffer
   constexpr size_t per_elem = TFFFT_SPLIT ? sizeof(cx<T>) + sizeof(T) : sizeof(cx<T>);
@@ -148,7 +137,7 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
   // while the tile computes; when slots for all E do not fit beside the
   // exchange buffer, the other LO_E are fetched into the exchange buffer as
   // soon as the tile's last exchange has drained it.
-  static constexpr size_t SMEM_MAX = (size_t)(L == 10 && sizeof(T) == 8 && THREADS <= 128 ? TFFFT_COL_SMEM_KB : 227) * 1024;
+  static constexpr size_t SMEM_MAX = 227 * 1024;
   static constexpr int PF_FIT = (int)((SMEM_MAX - X_BYTES) / (sizeof(cx<T>) * THREADS));
   static constexpr int PF_E = !PREFETCH ? 0 : (PF_FIT < Shape<L>::E ? PF_FIT : Shape<L>::E);
   static constexpr int LO_E = PREFETCH ? Shape<L>::E - PF_E : 0;
