@@ -392,7 +392,14 @@ r2c_rows_kernel(const RowParams prm) {
 
   ST::run(sm, v, tt, b, tw);
   if constexpr (SH::P > 1) __syncthreads();  // last exchange reads done before reuse
-  ST::store_natural(sm, v, tt, b);
+  // natural-order outputs, UNPADDED: the post-processing reads contiguous runs
+  // of k and of N - k, and a reversed run straddles the exchange layout's pad
+  // slots (2-way bank conflicts on every read of N - k)
+  cx<T>* zr = sm + b * RC::S;
+#pragma unroll
+  for (int u = 0; u < SH::E / SH::RL; ++u)
+#pragma unroll
+    for (int m = 0; m < SH::RL; ++m) zr[SH::out_elem(tt, u, m)] = v[u * SH::RL + m];
   __syncthreads();
   if (!valid) return;
 
@@ -403,12 +410,12 @@ r2c_rows_kernel(const RowParams prm) {
     const int k = tt + SH::TPT * q;
     cx<T> X;
     if (k == 0) {
-      const cx<T> z0 = sm[ST::sidx(b, 0)];
+      const cx<T> z0 = zr[0];
       X = {z0.x + z0.y, T(0)};
       out[N] = cx<T>{z0.x - z0.y, T(0)};
     } else {
-      const cx<T> A = sm[ST::sidx(b, k)];
-      const cx<T> Bz = sm[ST::sidx(b, N - k)];
+      const cx<T> A = zr[k];
+      const cx<T> Bz = zr[N - k];
       const cx<T> S = {A.x + Bz.x, A.y - Bz.y};   // A + conj(B)
       const cx<T> D = {A.x - Bz.x, A.y + Bz.y};   // A - conj(B)
       const cx<T> Tt = cmul(D, ldg_cx(twp + k));
@@ -450,6 +457,9 @@ c2r_rows_kernel(const RowParams prm) {
   // as an integer: one IMNMX per element instead of a ~8-instruction double
   // fmax.  The record stores the word with an all-ones low half, an upper bound
   // within 2^-20 relative of the exact maximum (the tolerance is 1e-9 n max|X|).
+  // the row in natural order, UNPADDED (reversed runs N - k stay bank-conflict
+  // free); the FFT's exchanges below use the padded Stockham layout
+  cx<T>* xr = sm + b * RC::S;
   constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
   constexpr int SEGS = SH::TPT / W;  // warp segments per row
   __shared__ int seg_m2[RC::B][SEGS];
@@ -467,18 +477,18 @@ c2r_rows_kernel(const RowParams prm) {
     const int k = tt + SH::TPT * q;
     const cx<T> X = in[k];
     m2h = max(m2h, m2hi(X));
-    sm[ST::sidx(b, k)] = X;
+    xr[k] = X;
   }
   if (tt == 0) {
-    cx<T> X0 = sm[ST::sidx(b, 0)];
+    cx<T> X0 = xr[0];
     cx<T> XN = in[N];
     m2h = max(m2h, m2hi(XN));
     e0 = fabs((double)X0.y);
     eN = fabs((double)XN.y);
     X0.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
     XN.y = T(0);
-    sm[ST::sidx(b, 0)] = X0;
-    sm[ST::sidx(b, N)] = XN;
+    xr[0] = X0;
+    xr[N] = XN;
   }
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) m2h = max(m2h, __shfl_xor_sync(0xffffffffu, m2h, o, W));
@@ -504,8 +514,8 @@ c2r_rows_kernel(const RowParams prm) {
 #pragma unroll
     for (int m = 0; m < SH::R0; ++m) {
       const int k = SH::in_elem(tt, u, m);
-      const cx<T> A = sm[ST::sidx(b, k)];
-      const cx<T> Bx = sm[ST::sidx(b, N - k)];
+      const cx<T> A = xr[k];
+      const cx<T> Bx = xr[N - k];
       const cx<T> S = {A.x + Bx.x, A.y - Bx.y};  // A + conj(B)
       const cx<T> D = {A.x - Bx.x, A.y + Bx.y};  // A - conj(B)
       const cx<T> Tt = cmulc(D, ldg_cx(twp + k)); // exp(+2 pi i k / n2) * D
