@@ -167,6 +167,14 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 __host__ __device__ constexpr int r2c_radix_bits(int L, int real_bytes) {
   return (L == 9 && real_bytes == 8) ? TFFFT_R2C_L9_F64_MB : 0;
 }
+// c2r likewise: radix 8 at 6 CTAs/SM, 3.14 ms per 1024^3 launch vs 3.23 ms
+// with radix 32x16 at 240 registers (profiles/r01s3/rows.txt)
+#ifndef TFFFT_C2R_L9_F64_MB
+#define TFFFT_C2R_L9_F64_MB 4
+#endif
+__host__ __device__ constexpr int c2r_radix_bits(int L, int real_bytes) {
+  return (L == 9 && real_bytes == 8) ? TFFFT_C2R_L9_F64_MB : 0;
+}
 
 template <int L, int MB = 0> struct RowCfg {
   static constexpr int TPT = Shape<L, MB>::TPT;
@@ -431,11 +439,13 @@ r2c_rows_kernel(const RowParams prm) {
 __device__ __forceinline__ unsigned long long ord(double x) { return __double_as_longlong(x); }
 
 template <typename T, int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::MINB_C2R)
+__global__ void __launch_bounds__(RowCfg<L, c2r_radix_bits(L, sizeof(T))>::THREADS,
+                                  RowCfg<L, c2r_radix_bits(L, sizeof(T))>::MINB_C2R)
 c2r_rows_kernel(const RowParams prm) {
-  using RC = RowCfg<L>;
-  using SH = Shape<L>;
-  using ST = Stockham<T, L, true, RC::S, RC::PS>;
+  constexpr int MB = c2r_radix_bits(L, sizeof(T));
+  using RC = RowCfg<L, MB>;
+  using SH = Shape<L, MB>;
+  using ST = Stockham<T, L, true, RC::S, RC::PS, false, 0, false, MB>;
   constexpr int N = SH::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);

@@ -80,8 +80,8 @@ static cudaError_t r2c_one(const RowParams& p, cudaStream_t s) {
 
 template <typename T, int L>
 static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
-  using RC = RowCfg<L>;
-  const size_t sm = row_smem_bytes<T, L>();
+  using RC = RowCfg<L, c2r_radix_bits(L, sizeof(T))>;
+  const size_t sm = row_smem_bytes<T, L, c2r_radix_bits(L, sizeof(T))>();
   auto k = c2r_rows_kernel<T, L>;
   static cudaError_t prep = prep_smem(k, sm);
   if (prep != cudaSuccess) return prep;

@@ -210,6 +210,7 @@ struct tffft_plan_s {
   void* tw1 = nullptr;
   void* tw2 = nullptr;   // row pass tables (c2r, fused stage 1)
   void* tw2r = nullptr;  // row pass tables in the r2c kernel's schedule
+  void* tw2c = nullptr;  // row pass tables in the c2r kernel's schedule
   void* tw2post = nullptr;
   unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles)
   double* row_stats = nullptr;          // per row records of the c2r kernel
@@ -324,8 +325,10 @@ static cudaError_t r2c_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_
 }
 static cudaError_t c2r_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_t s) {
   pl->launches++;
-  return pl->dtype == TFFFT_F64 ? launch_c2r_rows<double>(pl->L2h, prm, s)
-                                : launch_c2r_rows<float>(pl->L2h, prm, s);
+  RowParams q = prm;
+  q.tw = pl->tw2c;  // the c2r kernel's own radix schedule (c2r_radix_bits)
+  return pl->dtype == TFFFT_F64 ? launch_c2r_rows<double>(pl->L2h, q, s)
+                                : launch_c2r_rows<float>(pl->L2h, q, s);
 }
 
 // local-fabric pull: chunk c copies `words` W-sized words from ptrs[2c] to ptrs[2c+1]
@@ -1091,6 +1094,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   TRY(upload_table(pass_table(pl->L1), dtype, &pl->tw1, &ws));
   TRY(upload_table(pass_table(pl->L2h), dtype, &pl->tw2, &ws));
   TRY(upload_table(pass_table(pl->L2h, r2c_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2r, &ws));
+  TRY(upload_table(pass_table(pl->L2h, c2r_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2c, &ws));
   TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
   CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
@@ -1199,7 +1203,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   if (!pl) return TFFFT_OK;
   cudaSetDevice(pl->comm->device);
   free_events(pl);
-  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2post);
+  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2c); cudaFree(pl->tw2post);
   cudaFree(pl->stats); cudaFree(pl->row_stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
   cudaFree(pl->band_dst);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
