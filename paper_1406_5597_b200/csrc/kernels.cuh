@@ -411,26 +411,34 @@ r2c_rows_kernel(const RowParams prm) {
   __syncthreads();
   if (!valid) return;
 
+  // Bins k and N - k come from the same pair (Z[k], Z[N-k]): with
+  // S = Z[k] + conj(Z[N-k]), D = Z[k] - conj(Z[N-k]), T = D w^k (w = e^{-2 pi i / n2}),
+  //   X[k]     = (S.x + T.y, S.y - T.x) / 2
+  //   X[N - k] = (S.x - T.y, -(S.y + T.x)) / 2   (w^{N-k} = -conj(w^k))
+  // so each thread reads every pair once and writes both bins.
   cx<T>* out = reinterpret_cast<cx<T>*>(prm.spec) + row * prm.n2c;
   const T half = T(0.5);
+  auto pair = [&](int k) {
+    const cx<T> A = zr[k];
+    const cx<T> Bz = zr[N - k];
+    const cx<T> S = {A.x + Bz.x, A.y - Bz.y};   // A + conj(B)
+    const cx<T> D = {A.x - Bz.x, A.y + Bz.y};   // A - conj(B)
+    const cx<T> Tt = cmul(D, ldg_cx(twp + k));
+    out[k] = cx<T>{half * (S.x + Tt.y), half * (S.y - Tt.x)};
+    if (N - k != k) out[N - k] = cx<T>{half * (S.x - Tt.y), -half * (S.y + Tt.x)};
+  };
 #pragma unroll
-  for (int q = 0; q < SH::E; ++q) {
-    const int k = tt + SH::TPT * q;
-    cx<T> X;
+  for (int q = 0; q < (SH::E > 1 ? SH::E / 2 : 1); ++q) {
+    const int k = tt + SH::TPT * q;  // k < N/2
     if (k == 0) {
       const cx<T> z0 = zr[0];
-      X = {z0.x + z0.y, T(0)};
+      out[0] = cx<T>{z0.x + z0.y, T(0)};
       out[N] = cx<T>{z0.x - z0.y, T(0)};
     } else {
-      const cx<T> A = zr[k];
-      const cx<T> Bz = zr[N - k];
-      const cx<T> S = {A.x + Bz.x, A.y - Bz.y};   // A + conj(B)
-      const cx<T> D = {A.x - Bz.x, A.y + Bz.y};   // A - conj(B)
-      const cx<T> Tt = cmul(D, ldg_cx(twp + k));
-      X = {half * (S.x + Tt.y), half * (S.y - Tt.x)};
+      pair(k);
     }
-    out[k] = X;
   }
+  if (tt == 0 && N >= 2) pair(N / 2);  // the self-paired middle bin
 }
 
 // ---------------------------------------------------------------------------
