@@ -466,47 +466,90 @@ c2r_rows_kernel(const RowParams prm) {
   const bool valid = row < prm.nrows;
   const cx<T>* in = reinterpret_cast<const cx<T>*>(prm.spec) + (valid ? row : 0) * prm.n2c;
 
-  // row -> shared memory, with the statistics of the Hermitian check: max |X|^2
-  // over the row (every thread), |Im X_0|, |Im X_N| (thread tt == 0 only).
+  // Hermitian pre-processing: the thread's pass-0 operands k = in_elem(...)
+  // and their partners N - k (contiguous forward / reversed runs per warp).
+  // Statistics of the Hermitian check on the way: max |X|^2 over the row
+  // (each k < N once, bin N by thread 0), |Im X_0|, |Im X_N| (thread 0).
   // Each row writes one plain 24-byte record (reduced per plane on request by
   // reduce_row_stats_kernel): atomics from the ~1000 rows of a plane in flight
   // would serialise on a few L2 addresses (measured +0.4 ms per 1024^3 launch).
-  // max |X|^2 is kept as the high word of the (non-negative) double, compared
-  // as an integer: one IMNMX per element instead of a ~8-instruction double
-  // fmax.  The record stores the word with an all-ones low half, an upper bound
-  // within 2^-20 relative of the exact maximum (the tolerance is 1e-9 n max|X|).
-  // the row in natural order, UNPADDED (reversed runs N - k stay bank-conflict
-  // free); the FFT's exchanges below use the padded Stockham layout
-  cx<T>* xr = sm + b * RC::S;
+  // float64: max |X|^2 is kept as the high word of the (non-negative) double,
+  // compared as an integer, one IMNMX per element; the record stores the word
+  // with an all-ones low half, an upper bound within 2^-20 relative of the
+  // exact maximum (the tolerance is 1e-9 n max|X|).  float32: max(|Re X|,
+  // |Im X|) compared as the float's bit pattern; the record 2 m^2 bounds
+  // max |X|^2 from above (within 2x), well inside the float32 tolerance.
   constexpr int W = SH::TPT < 32 ? SH::TPT : 32;
   constexpr int SEGS = SH::TPT / W;  // warp segments per row
   __shared__ int seg_m2[RC::B][SEGS];
-  // float32: max(|Re X|, |Im X|) compared as the (non-negative) float's bit
-  // pattern, no conversion to double per element; the record 2 m^2 bounds
-  // max |X|^2 from above (within 2x), well inside the float32 tolerance.
   int m2h = 0;
   double e0 = 0.0, eN = 0.0;
   auto m2hi = [](cx<T> X) {
     if constexpr (sizeof(T) == 4) return __float_as_int(fmaxf(fabsf(X.x), fabsf(X.y)));
     else return __double2hiint(fma((double)X.x, (double)X.x, (double)X.y * X.y));
   };
+  // the pre-processed pass-0 operand from the bin pair (A = X_k, B = X_{N-k})
+  auto pre = [&](cx<T> A, cx<T> Bx, int k) -> cx<T> {
+    const cx<T> S = {A.x + Bx.x, A.y - Bx.y};  // A + conj(B)
+    const cx<T> D = {A.x - Bx.x, A.y + Bx.y};  // A - conj(B)
+    const cx<T> Tt = cmulc(D, ldg_cx(twp + k)); // exp(+2 pi i k / n2) * D
+    return {S.x - Tt.y, S.y + Tt.x};
+  };
+  cx<T> v[SH::E];
+  if constexpr (sizeof(T) == 8) {
+    // float64 (radix-8 schedule): pairs straight from global memory, 1024^3
+    // launch 3.14 -> 2.97 ms against staging the row in shared memory
 #pragma unroll
-  for (int q = 0; q < SH::E; ++q) {
-    const int k = tt + SH::TPT * q;
-    const cx<T> X = in[k];
-    m2h = max(m2h, m2hi(X));
-    xr[k] = X;
-  }
-  if (tt == 0) {
-    cx<T> X0 = xr[0];
-    cx<T> XN = in[N];
-    m2h = max(m2h, m2hi(XN));
-    e0 = fabs((double)X0.y);
-    eN = fabs((double)XN.y);
-    X0.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
-    XN.y = T(0);
-    xr[0] = X0;
-    xr[N] = XN;
+    for (int u = 0; u < SH::E / SH::R0; ++u)
+#pragma unroll
+      for (int m = 0; m < SH::R0; ++m) {
+        const int k = SH::in_elem(tt, u, m);
+        cx<T> A = ldg_cx(in + k);
+        m2h = max(m2h, m2hi(A));
+        cx<T> Bx;
+        if (k == 0) {  // c2r uses only the real part of the DC / Nyquist bins
+          Bx = ldg_cx(in + N);
+          m2h = max(m2h, m2hi(Bx));
+          e0 = fabs((double)A.y);
+          eN = fabs((double)Bx.y);
+          A.y = T(0);
+          Bx.y = T(0);
+        } else {
+          Bx = ldg_cx(in + (N - k));
+        }
+        v[u * SH::R0 + m] = pre(A, Bx, k);
+      }
+  } else {
+    // float32 (radix-32 schedule): the row staged in shared memory in natural
+    // order, UNPADDED (reversed runs N - k stay bank-conflict free); 1.43 ms
+    // against 1.83 ms for the global pair reads
+    cx<T>* xr = sm + b * RC::S;
+#pragma unroll
+    for (int q = 0; q < SH::E; ++q) {
+      const int k = tt + SH::TPT * q;
+      const cx<T> X = in[k];
+      m2h = max(m2h, m2hi(X));
+      xr[k] = X;
+    }
+    if (tt == 0) {
+      cx<T> X0 = xr[0];
+      cx<T> XN = in[N];
+      m2h = max(m2h, m2hi(XN));
+      e0 = fabs((double)X0.y);
+      eN = fabs((double)XN.y);
+      X0.y = T(0);  // c2r uses only the real part of the DC / Nyquist bins
+      XN.y = T(0);
+      xr[0] = X0;
+      xr[N] = XN;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < SH::E / SH::R0; ++u)
+#pragma unroll
+      for (int m = 0; m < SH::R0; ++m) {
+        const int k = SH::in_elem(tt, u, m);
+        v[u * SH::R0 + m] = pre(xr[k], xr[N - k], k);
+      }
   }
 #pragma unroll
   for (int o = W / 2; o > 0; o >>= 1) m2h = max(m2h, __shfl_xor_sync(0xffffffffu, m2h, o, W));
@@ -525,21 +568,7 @@ c2r_rows_kernel(const RowParams prm) {
     rec[1] = fmax(e0, eN);
     rec[2] = e0 + eN;
   }
-
-  cx<T> v[SH::E];
-#pragma unroll
-  for (int u = 0; u < SH::E / SH::R0; ++u)
-#pragma unroll
-    for (int m = 0; m < SH::R0; ++m) {
-      const int k = SH::in_elem(tt, u, m);
-      const cx<T> A = xr[k];
-      const cx<T> Bx = xr[N - k];
-      const cx<T> S = {A.x + Bx.x, A.y - Bx.y};  // A + conj(B)
-      const cx<T> D = {A.x - Bx.x, A.y + Bx.y};  // A - conj(B)
-      const cx<T> Tt = cmulc(D, ldg_cx(twp + k)); // exp(+2 pi i k / n2) * D
-      v[u * SH::R0 + m] = {S.x - Tt.y, S.y + Tt.x};
-    }
-  __syncthreads();
+  if constexpr (sizeof(T) == 4) __syncthreads();  // the staged row is consumed before the exchanges reuse it
 
   ST::run(sm, v, tt, b, tw);
   if (!valid) return;
