@@ -95,6 +95,16 @@ enum {
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* plan);
+/* Fused exchange on an NCCL communicator (TFFFT_FLAG_PEER_STORES, p > 1): each
+ * rank exports a CUDA IPC handle of its landing buffer, the handles are
+ * all-gathered by the caller (rank order, 64 bytes each), and attach_peers
+ * maps the peers' landing buffers so the stage-1 / stage-3' epilogues store
+ * every peer band straight into the peer's memory over NVLink; the exchange is
+ * then a one-int ncclAllReduce barrier (exchange.py:263-290 with the strided
+ * datatype realised by the stores themselves).  Collective: every rank of the
+ * communicator must call attach_peers. */
+int tffft_plan_landing_handle(tffft_plan_t plan, uint8_t handle[64]);
+int tffft_plan_attach_peers(tffft_plan_t plan, const uint8_t* handles /* p * 64 bytes */);
 /* algorithm flags actually in effect (a flag is dropped when the grid has no such kernel) */
 int tffft_plan_flags(tffft_plan_t plan, int* flags);
 /* device bytes owned by the plan (staging, twiddles, statistics) */

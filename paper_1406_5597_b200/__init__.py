@@ -14,7 +14,7 @@ from .streaming import HostPairStream
 from .fields import forward_batch, inverse_batch, radial_wavenumber, turbulence_spectrum
 from .layout import (DistAxis, GlobalGrid, RealSlab, SlabLayout, SpectralSlab, SpectralTag,
                      TwoLevelStride, column_stride_descriptor, owned_range, spectral_offset, validate)
-from .transport import (CommMode, CommPattern, CopyCounter, Endpoint, init_nccl_endpoint,
+from .transport import (CommMode, CommPattern, CopyCounter, Endpoint, allgather_handles, init_nccl_endpoint,
                         make_communicators, run_spmd)
 
 __version__ = "0.1.0"

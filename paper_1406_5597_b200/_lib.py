@@ -32,6 +32,8 @@ _SIGS = {
     "tffft_plan_create_ex": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
                                         _c.c_void_p, _c.POINTER(_c.c_void_p)]),
     "tffft_plan_flags": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
+    "tffft_plan_landing_handle": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
+    "tffft_plan_attach_peers": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "tffft_plan_workspace_bytes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_size_t)]),
     "tffft_plan_sizes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int64), _c.POINTER(_c.c_int64)]),
     "tffft_plan_destroy": (_c.c_int, [_c.c_void_p]),

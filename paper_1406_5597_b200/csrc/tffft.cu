@@ -83,6 +83,8 @@ struct NcclApi {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   // optional (NCCL >= 2.28): the COLLECTIVE pattern's single all-to-all
   ncclResult_t (*AlltoAll)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
 };
 
 static NcclApi& nccl() {
@@ -102,7 +104,7 @@ static NcclApi& nccl() {
   api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name));   \
   if (!api.name) { api.err = "missing symbol nccl" #name; return; }
     LOAD(GetUniqueId) LOAD(CommInitRank) LOAD(CommDestroy) LOAD(CommAbort) LOAD(CommGetAsyncError)
-    LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd) LOAD(GetErrorString)
+    LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd) LOAD(GetErrorString) LOAD(AllReduce)
 #undef LOAD
     api.AlltoAll = reinterpret_cast<decltype(api.AlltoAll)>(dlsym(h, "ncclAlltoAll"));
     api.loaded = true;
@@ -206,6 +208,9 @@ struct tffft_plan_s {
   void* landing = nullptr;   // incoming peer bands [q][i][j][k]
   void** band_dst = nullptr; // device: destination block of each outgoing band (p pointers)
   bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
+  bool peer_stores_wanted = false;  // NCCL communicator: peer stores once the peers' landing buffers are attached
+  std::vector<void*> peer_landing;  // NCCL + peer stores: rank q's landing buffer, opened through CUDA IPC
+  int* barrier_word = nullptr;      // NCCL + peer stores: one-int all-reduce used as a stream-ordered barrier
   void* tw0 = nullptr;
   void* tw1 = nullptr;
   void* tw2 = nullptr;   // row pass tables (c2r, fused stage 1)
@@ -700,8 +705,20 @@ static uint64_t wire_bytes(tffft_plan_t pl) {
 // peer must have finished pulling from our staging; with peer stores, every
 // peer must have finished reading its landing buffer (the host barrier makes
 // sure each peer recorded that event for the previous exchange).
+// Stream-ordered barrier over an NCCL communicator: a one-int all-reduce.  It
+// completes on this rank only after every rank's preceding kernels have
+// completed, so their peer stores into our landing buffer are visible (or,
+// before a producing stage, every peer has finished reading its landing
+// buffer).
+static int nccl_barrier(tffft_plan_t pl, cudaStream_t s) {
+  NcclApi& api = nccl();
+  NCCL_TRY(api.AllReduce(pl->barrier_word, pl->barrier_word, 1, ncclInt32, ncclSum, pl->comm->nccl, s));
+  return TFFFT_OK;
+}
+
 static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
-  if (pl->p == 1 || pl->comm->is_nccl) return TFFFT_OK;
+  if (pl->p == 1) return TFFFT_OK;
+  if (pl->comm->is_nccl) return pl->peer_stores ? nccl_barrier(pl, s) : TFFFT_OK;
   auto& slot = pl->comm->fabric->slot(pl->seq);
   if (pl->peer_stores) TRY(pl->comm->fabric->barrier());
   for (int q = 0; q < pl->p; ++q)
@@ -711,7 +728,7 @@ static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
 
 // peer stores: this rank has consumed its landing buffer
 static int fabric_landing_consumed(tffft_plan_t pl, cudaStream_t s) {
-  if (!pl->peer_stores) return TFFFT_OK;
+  if (!pl->peer_stores || pl->comm->is_nccl) return TFFFT_OK;  // NCCL: the next guard barrier covers it
   CUDA_TRY(cudaEventRecord(pl->comm->fabric->slot(pl->seq).done[pl->rank], s));
   return TFFFT_OK;
 }
@@ -721,14 +738,17 @@ static int build_band_dst(tffft_plan_t pl) {
   const size_t band = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
   std::vector<void*> h(pl->p, nullptr);
   for (int q = 0; q < pl->p; ++q) {
-    if (pl->peer_stores) {
+    if (pl->peer_stores && pl->comm->is_nccl) {
+      h[q] = q == pl->rank ? static_cast<char*>(pl->staging) + (size_t)q * band
+                           : static_cast<char*>(pl->peer_landing[q]) + (size_t)pl->rank * band;
+    } else if (pl->peer_stores) {
       auto& slot = pl->comm->fabric->slot(pl->seq);
       h[q] = static_cast<char*>(slot.landing[q]) + (size_t)pl->rank * band;  // rank q's landing block for us
     } else {
       h[q] = static_cast<char*>(pl->staging) + (size_t)q * band;
     }
   }
-  CUDA_TRY(cudaMalloc(&pl->band_dst, sizeof(void*) * pl->p));
+  if (!pl->band_dst) CUDA_TRY(cudaMalloc(&pl->band_dst, sizeof(void*) * pl->p));
   CUDA_TRY(cudaMemcpy(pl->band_dst, h.data(), sizeof(void*) * pl->p, cudaMemcpyHostToDevice));
   return TFFFT_OK;
 }
@@ -742,6 +762,13 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
   (void)spec;
   if (pl->p == 1) return TFFFT_OK;
   const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
+  if (pl->peer_stores && pl->comm->is_nccl) {
+    // the epilogue already stored every band into its peer's landing buffer
+    // over NVLink (CUDA IPC mapping): the exchange is the barrier
+    TRY(nccl_barrier(pl, s));
+    pl->counters[1] += wire_bytes(pl);
+    return TFFFT_OK;
+  }
   if (pl->peer_stores) {
     // the epilogue already stored every band into its peer's landing buffer:
     // the exchange is the barrier after which every rank's stores are visible
@@ -1044,6 +1071,38 @@ int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   return TFFFT_OK;
 }
 
+int tffft_plan_landing_handle(tffft_plan_t pl, uint8_t handle[64]) {
+  if (!pl || !handle) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (!pl->comm->is_nccl || pl->p == 1 || !pl->landing)
+    return fail(TFFFT_ERR_CONFIGURATION, "landing handles exist for NCCL plans with p > 1 only");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, pl->landing));
+  memcpy(handle, &h, 64);
+  return TFFFT_OK;
+}
+
+int tffft_plan_attach_peers(tffft_plan_t pl, const uint8_t* handles) {
+  if (!pl || !handles) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (!pl->comm->is_nccl || pl->p == 1 || !pl->peer_stores_wanted)
+    return fail(TFFFT_ERR_CONFIGURATION, "attach_peers needs an NCCL plan with p > 1 created with TFFFT_FLAG_PEER_STORES");
+  if (pl->peer_stores) return fail(TFFFT_ERR_PROTOCOL, "peers already attached");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  pl->peer_landing.assign(pl->p, nullptr);
+  for (int q = 0; q < pl->p; ++q) {
+    if (q == pl->rank) { pl->peer_landing[q] = pl->landing; continue; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * (size_t)q, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(&pl->peer_landing[q], h, cudaIpcMemLazyEnablePeerAccess));
+  }
+  CUDA_TRY(cudaMalloc(&pl->barrier_word, sizeof(int)));
+  CUDA_TRY(cudaMemset(pl->barrier_word, 0, sizeof(int)));
+  pl->peer_stores = true;
+  TRY(build_band_dst(pl));
+  return TFFFT_OK;
+}
+
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* out) {
   // TMA column passes: explicit flag = every supported pass; environment
@@ -1111,7 +1170,9 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     CUDA_TRY(cudaMalloc(&pl->staging, sb));
     CUDA_TRY(cudaMalloc(&pl->landing, sb));
     ws += 2 * sb;
-    if (!comm->is_nccl) {
+    if (comm->is_nccl) {
+      pl->peer_stores_wanted = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
+    } else {
       const size_t nptr = 2 * (size_t)(p - 1);
       CUDA_TRY(cudaMalloc(&pl->pull_ptrs, nptr * sizeof(void*)));
       ws += nptr * sizeof(void*);
@@ -1209,6 +1270,9 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
+  for (size_t q = 0; q < pl->peer_landing.size(); ++q)
+    if (pl->peer_landing[q] && (int)q != pl->rank) cudaIpcCloseMemHandle(pl->peer_landing[q]);
+  cudaFree(pl->barrier_word);
   for (auto e : pl->s1_ev_row) cudaEventDestroy(e);
   for (auto e : pl->s1_ev_col) cudaEventDestroy(e);
   if (pl->s1_aux) cudaStreamDestroy(pl->s1_aux);

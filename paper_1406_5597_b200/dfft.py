@@ -157,6 +157,14 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
         dev = torch.device("cuda", comm.device)
         work1 = torch.empty((grid.n0 // p) * grid.n1 * grid.n2c, dtype=cdt, device=dev)
         real_out = torch.empty((grid.n0 // p) * grid.n1 * grid.n2, dtype=rdt, device=dev)
+    if comm.kind == "nccl" and comm.p > 1 and (flags >= 0 and flags & ALGORITHM_FLAGS["peer_stores"]):
+        # fused exchange over NVLink: map every peer's landing buffer (CUDA IPC)
+        from .transport import allgather_handles
+        buf = ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib().tffft_plan_landing_handle(h, buf))
+        allh = allgather_handles(buf.raw, comm.rank, comm.p)
+        with torch.cuda.device(comm.device):
+            _lib.check(_lib.lib().tffft_plan_attach_peers(h, allh))
     return FftPlan(
         grid=grid, comm=comm, strategy=strategy, comm_pattern=comm_pattern,
         real_layout=SlabLayout(grid, p, rank, DistAxis.REAL_AXIS0),

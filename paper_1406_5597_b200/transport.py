@@ -31,6 +31,7 @@ __all__ = [
     "make_communicators",
     "run_spmd",
     "init_nccl_endpoint",
+    "allgather_handles",
 ]
 
 
@@ -175,3 +176,22 @@ def init_nccl_endpoint(device: int | None = None) -> Endpoint:
     h = ctypes.c_void_p()
     _lib.check(_lib.lib().tffft_comm_init_rank(p, rank, bytes(uid), dev, ctypes.byref(h)))
     return Endpoint(h.value, rank, p, dev, "nccl")
+
+
+def allgather_handles(handle: bytes, rank: int, p: int) -> bytes:
+    """All-gather one fixed-size handle per rank over the default
+    torch.distributed group and return the concatenation in RANK order (the
+    layout tffft_plan_attach_peers expects).  Every rank must call it."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise ConfigurationError("torch.distributed is not initialised")
+    if dist.get_world_size() != p or dist.get_rank() != rank:
+        raise ConfigurationError(f"process group (rank {dist.get_rank()} of {dist.get_world_size()}) does not match "
+                                 f"the communicator (rank {rank} of {p})")
+    got: list = [None] * p
+    dist.all_gather_object(got, bytes(handle))
+    sizes = {len(h) for h in got}
+    if sizes != {len(handle)}:
+        raise TransportError(f"handle sizes differ across ranks: {sorted(sizes)}")
+    return b"".join(got)

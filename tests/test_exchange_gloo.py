@@ -83,3 +83,70 @@ def test_exchange_schedule_over_gloo(world, shape, pattern):
     res = dict(q.get(timeout=5) for _ in range(world))
     assert all(p.exitcode == 0 for p in procs)
     assert all(res[r] for r in range(world)), res
+
+
+def _peer_store_worker(rank, world, port, shape, landings, q):
+    """Fused exchange over NCCL (peer stores through CUDA IPC mappings), host
+    protocol on CPU: every rank publishes a 64-byte handle of its landing
+    buffer, tf.allgather_handles returns them in rank order, and the stage-1
+    epilogue's destination for band q is `landing of rank q + rank * band`
+    (tffft.cu build_band_dst).  Shared-memory tensors stand in for the mapped
+    peer buffers, dist.barrier for the one-int ncclAllReduce barrier."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1406_5597_b200 as tf
+
+        n0, n1, n2 = shape
+        n0p, n1p, n2c = n0 // world, n1 // world, n2 // 2 + 1
+        band = n0p * n1p * n2c
+        # a handle: 64 bytes naming this rank's landing buffer (index + padding)
+        handle = rank.to_bytes(4, "little") + bytes(60)
+        allh = tf.allgather_handles(handle, rank, world)
+        assert len(allh) == 64 * world
+        peers = [int.from_bytes(allh[64 * r:64 * r + 4], "little") for r in range(world)]
+        assert peers == list(range(world))
+        for _ in range(2):  # two calls: the guard barrier orders reuse of the landing buffers
+            dist.barrier()  # guard: every peer has consumed its landing buffer
+            x = oracle.normal_field(shape, 13)
+            s1 = oracle.stage1_forward(x[rank * n0p:(rank + 1) * n0p])
+            spec, staging = oracle.stage1_band_staging(s1, world, rank)
+            stg = staging.reshape(world, band)
+            for qq in range(world):  # epilogue stores: band qq -> landing of rank qq, block `rank`
+                if qq != rank:
+                    dst = landings[peers[qq]].numpy().reshape(world, band)
+                    dst[rank] = stg[qq]
+            dist.barrier()  # the exchange: every rank's stores are visible
+            lnd = landings[rank].numpy().reshape(world, n0p, n1p, n2c)
+            out3 = spec.reshape(n0p, world, n1p, n2c).copy()
+            for s_ in range(world):
+                if s_ != rank:
+                    out3[:, s_] = lnd[s_]
+            out = out3.reshape(-1)
+            oracle.stage3(out, n0, n1, n2, world, inverse=False)
+            ref = oracle.forward_all(x, world)[rank]
+            ok = bool(np.array_equal(out.view(np.float64), ref.view(np.float64)))
+            if not ok:
+                break
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (8, 8, 8)), (4, (8, 16, 4))])
+def test_peer_store_protocol_over_gloo(world, shape):
+    n0, n1, n2 = shape
+    band = (n0 // world) * (n1 // world) * (n2 // 2 + 1)
+    landings = [torch.zeros(world * band, dtype=torch.complex128).share_memory_() for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_store_worker, args=(r, world, port, shape, landings, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(res[r] for r in range(world)), res
