@@ -6,7 +6,7 @@
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
-#include "col_ws.cuh"
+#include "col_tma.cuh"
 
 namespace tffft {
 

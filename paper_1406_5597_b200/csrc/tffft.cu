@@ -29,7 +29,7 @@
 #include "fourstep.cuh"
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
-#include "col_ws.cuh"
+#include "col_tma.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 
@@ -233,12 +233,6 @@ struct tffft_plan_s {
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
   int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 stage 3 only
-  // stage 1 pipelined over plane chunks on two streams (row kernel on s1_aux,
-  // column kernel on the caller's stream): a chunk's intermediate stays in L2
-  int s1_chunk = 0;      // planes per chunk (0 = whole slab, one launch per kernel)
-  int s1_depth = 2;      // row chunks in flight ahead of the column kernel
-  cudaStream_t s1_aux = nullptr;
-  std::vector<cudaEvent_t> s1_ev_row, s1_ev_col;
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -453,7 +447,7 @@ static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const
   return TFFFT_OK;
 }
 
-// Column pass through the TMA-fed column kernel (col_ws.cuh): `ngrp` groups
+// Column pass through the TMA-fed column kernel (col_tma.cuh): `ngrp` groups
 // of `cols` contiguous columns, column elements `rstride` apart, groups
 // `gstride` apart (elements).  Sets *done = false when the shape has no TMA
 // path (the caller falls back to col_fft_kernel).
@@ -630,38 +624,6 @@ static RowParams row_params(tffft_plan_t pl, void* real, void* spec, int plane0 
   r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
   r.row_stats = pl->row_stats + 3 * row0;
   return r;
-}
-
-// Stage 1 / 1' over plane chunks of pl->s1_chunk planes, two streams:
-//   forward : aux  r2c(c) -> ev_row[c]          main: wait ev_row[c], columns(c) -> ev_col[c]
-//   inverse : main columns'(c) -> ev_col[c]      aux : wait ev_col[c], c2r(c) -> ev_row[c]
-// The producer of chunk c + depth waits for the consumer of chunk c, so at most
-// depth + 1 chunks of intermediate planes are live: they stay in L2 between the
-// row and column kernels, and the two kernels fill each other's tails.
-static int stage1_pipelined(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaStream_t s) {
-  const int K = pl->s1_chunk, nch = (pl->n0p + K - 1) / K, D = pl->s1_depth;
-  const int R = (int)pl->s1_ev_row.size();
-  cudaStream_t a = pl->s1_aux;
-  cudaStream_t prod = fwd ? a : s, cons = fwd ? s : a;
-  CUDA_TRY(cudaEventRecord(pl->s1_ev_col[R - 1], s));  // fork: aux ordered after everything before
-  CUDA_TRY(cudaStreamWaitEvent(a, pl->s1_ev_col[R - 1], 0));
-  for (int c = 0; c < nch; ++c) {
-    const int p0 = c * K, np = std::min(K, pl->n0p - p0);
-    cudaEvent_t evp = pl->s1_ev_row[c % (R - 1)], evc = pl->s1_ev_col[c % (R - 1)];
-    if (c >= D) CUDA_TRY(cudaStreamWaitEvent(prod, pl->s1_ev_col[(c - D) % (R - 1)], 0));
-    if (fwd) CUDA_TRY(r2c_launch(pl, row_params(pl, real, spec, p0, np), prod));
-    else TRY(stage1_columns(pl, spec, true, prod, p0, np));
-    CUDA_TRY(cudaEventRecord(evp, prod));
-    CUDA_TRY(cudaStreamWaitEvent(cons, evp, 0));
-    if (fwd) TRY(stage1_columns(pl, spec, false, cons, p0, np));
-    else CUDA_TRY(c2r_launch(pl, row_params(pl, real, spec, p0, np), cons));
-    CUDA_TRY(cudaEventRecord(evc, cons));
-  }
-  if (!fwd) {  // join: the caller's stream continues after the last c2r
-    CUDA_TRY(cudaEventRecord(pl->s1_ev_row[R - 1], a));
-    CUDA_TRY(cudaStreamWaitEvent(s, pl->s1_ev_row[R - 1], 0));
-  }
-  return TFFFT_OK;
 }
 
 // fused stage 1 / 1': one persistent kernel per direction, planes stay in L2
@@ -1219,23 +1181,6 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
     }
   }
-  {
-    static const char* env_k = getenv("TFFFT_S1_CHUNK");
-    static const char* env_d = getenv("TFFFT_S1_DEPTH");
-    const int K = env_k ? atoi(env_k) : 0;
-    if (K > 0 && !pl->s1_fused && strategy == 0 && K < pl->n0p) {
-      pl->s1_chunk = K;
-      pl->s1_depth = env_d ? std::max(1, atoi(env_d)) : 2;
-      CUDA_TRY(cudaStreamCreateWithFlags(&pl->s1_aux, cudaStreamNonBlocking));
-      const int R = pl->s1_depth + 2;
-      pl->s1_ev_row.resize(R);
-      pl->s1_ev_col.resize(R);
-      for (int i = 0; i < R; ++i) {
-        CUDA_TRY(cudaEventCreateWithFlags(&pl->s1_ev_row[i], cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&pl->s1_ev_col[i], cudaEventDisableTiming));
-      }
-    }
-  }
   pl->workspace = ws;
   *out = pl.release();
   return TFFFT_OK;
@@ -1273,9 +1218,6 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   for (size_t q = 0; q < pl->peer_landing.size(); ++q)
     if (pl->peer_landing[q] && (int)q != pl->rank) cudaIpcCloseMemHandle(pl->peer_landing[q]);
   cudaFree(pl->barrier_word);
-  for (auto e : pl->s1_ev_row) cudaEventDestroy(e);
-  for (auto e : pl->s1_ev_col) cudaEventDestroy(e);
-  if (pl->s1_aux) cudaStreamDestroy(pl->s1_aux);
   delete pl;
   return TFFFT_OK;
 }
@@ -1314,8 +1256,6 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
   TRY(fabric_guard_staging(pl, s));
   if (pl->s1_fused) {
     TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
-  } else if (pl->s1_chunk > 0) {
-    TRY(stage1_pipelined(pl, const_cast<void*>(real_in), spec_out, true, s));
   } else {
     CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
     TRY(stage1_columns(pl, spec_out, false, s));
@@ -1371,9 +1311,6 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   // stage 1' (dfft.py:206-209)
   if (pl->s1_fused) {
     TRY(stage1_fused(pl, real_out, spec, false, s));
-  } else if (pl->s1_chunk > 0) {
-    TRY(stage1_pipelined(pl, real_out, spec, false, s));
-    TRY(fabric_landing_consumed(pl, s));
   } else {
     TRY(stage1_columns(pl, spec, true, s));
     TRY(fabric_landing_consumed(pl, s));

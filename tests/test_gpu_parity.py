@@ -387,7 +387,7 @@ TMA_CASES = [((512, 8, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((512, 
 @pytest.mark.parametrize("shape,p", TMA_CASES, ids=lambda v: str(v))
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_tma_column_kernel_bitwise(shape, p, dtype):
-    """TMA-fed column passes (col_ws.cuh, lengths 512 / 1024, p = 1): the same
+    """TMA-fed column passes (col_tma.cuh, lengths 512 / 1024, p = 1): the same
     Stockham arithmetic as the cp.async kernel, so spectra and inverse outputs
     are bitwise identical to the default kernels, and within tolerance of the
     oracle.  Covers partial tiles (columns not a multiple of the box width),
