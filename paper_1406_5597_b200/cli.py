@@ -263,7 +263,7 @@ def _add_common(sub, default_mode: str) -> None:
     command-line compatibility only: GPU ranks always run as concurrent host
     threads (the reference's SERIAL turnstile is a scheduling device of its
     simulated fabric)."""
-    sub.add_argument("--comm", type=CommPattern, choices=list(CommPattern), default=CommPattern.PAIRWISE,
+    sub.add_argument("--comm", type=CommPattern, choices=list(CommPattern), default=CommPattern.PAIRWISE, metavar="{pairwise,collective}",
                      help="all-to-all pattern: pairwise or collective (default pairwise)")
     sub.add_argument("--mode", choices=["threaded", "serial"], default=default_mode,
                      help="accepted for compatibility; ranks always run as threads")
