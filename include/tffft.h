@@ -63,6 +63,9 @@ int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tff
  * in-process multi-rank fabric, transport.py:188-302).  Each endpoint is
  * driven by its own host thread; forward/inverse are collectives. */
 int tffft_comm_init_local(int p, int device, tffft_comm_t* comms);
+/* asynchronous communicator failure (ncclCommGetAsyncError) as TFFFT_ERR_TRANSPORT;
+ * TFFFT_OK for a healthy or local communicator (transport.py:209-219 abort propagation) */
+int tffft_comm_check(tffft_comm_t comm);
 int tffft_comm_rank(tffft_comm_t comm, int* rank);
 int tffft_comm_size(tffft_comm_t comm, int* p);
 int tffft_comm_device(tffft_comm_t comm, int* device);

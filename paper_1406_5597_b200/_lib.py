@@ -22,6 +22,7 @@ _SIGS = {
     "tffft_get_unique_id": (_c.c_int, [_c.c_char_p]),
     "tffft_comm_init_rank": (_c.c_int, [_c.c_int, _c.c_int, _c.c_char_p, _c.c_int, _c.POINTER(_c.c_void_p)]),
     "tffft_comm_init_local": (_c.c_int, [_c.c_int, _c.c_int, _c.POINTER(_c.c_void_p)]),
+    "tffft_comm_check": (_c.c_int, [_c.c_void_p]),
     "tffft_comm_rank": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_comm_size": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_comm_device": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),

@@ -720,9 +720,23 @@ static int build_band_dst(tffft_plan_t pl) {
 // it; the next FFT stage reads the landing buffer through the STRIDED_INPLACE
 // addressing, so no rearrangement pass follows.  One send and one receive per
 // peer (the reference posts one strided LayoutDescriptor per peer).
+// Failure detection: an asynchronous NCCL error (a peer died,
+// a network fault) surfaces as TFFFT_ERR_TRANSPORT on the next exchange, like
+// the reference fabric's abort propagation (transport.py:209-219, 446-467).
+static int nccl_async_check(tffft_comm_t c) {
+  if (!c->is_nccl || c->p == 1 || !c->nccl) return TFFFT_OK;
+  NcclApi& api = nccl();
+  ncclResult_t st = ncclSuccess;
+  NCCL_TRY(api.CommGetAsyncError(c->nccl, &st));
+  if (st != ncclSuccess && st != ncclInProgress)
+    return fail(TFFFT_ERR_TRANSPORT, "NCCL communicator failed asynchronously: %s", api.GetErrorString(st));
+  return TFFFT_OK;
+}
+
 static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
   (void)spec;
   if (pl->p == 1) return TFFFT_OK;
+  TRY(nccl_async_check(pl->comm));
   const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
   if (pl->peer_stores && pl->comm->is_nccl) {
     // the epilogue already stored every band into its peer's landing buffer
@@ -975,6 +989,11 @@ int tffft_comm_init_local(int p, int device, tffft_comm_t* comms) {
     comms[r] = c;
   }
   return TFFFT_OK;
+}
+
+int tffft_comm_check(tffft_comm_t c) {
+  if (!c) return fail(TFFFT_ERR_CONFIGURATION, "null communicator");
+  return nccl_async_check(c);
 }
 
 int tffft_comm_rank(tffft_comm_t c, int* r) {

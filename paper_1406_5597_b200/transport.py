@@ -97,6 +97,11 @@ class Endpoint:
         elif self.p > 1 and torch.distributed.is_initialized():
             torch.distributed.barrier()
 
+    def check(self) -> None:
+        """Raise TransportError if the communicator failed asynchronously
+        (NCCL: ncclCommGetAsyncError); a no-op for the local fabric."""
+        _lib.check(_lib.lib().tffft_comm_check(self.handle))
+
     def abort(self) -> None:
         if self._host_barrier is not None:
             self._host_barrier.abort()

@@ -113,3 +113,21 @@ def test_status_codes_map_to_reference_exceptions():
     assert STATUS_TO_ERROR[4] is tf.ContractError
     assert STATUS_TO_ERROR[7] is tf.ConsistencyError
     assert issubclass(tf.ConfigurationError, ValueError) and issubclass(tf.ContractError, tf.SlabFftError)
+
+
+def test_comm_check_local_fabric_is_healthy():
+    """tffft_comm_check (SURVEY §5 failure detection) on the local fabric:
+    nothing asynchronous can fail, the call returns TFFFT_OK; a null
+    communicator is a ConfigurationError."""
+    import paper_1406_5597_b200 as tf
+    lib = _lib.lib()
+    arr = (ctypes.c_void_p * 2)()
+    _lib.check(lib.tffft_comm_init_local(2, 0, arr))
+    try:
+        for r in range(2):
+            assert lib.tffft_comm_check(arr[r]) == 0
+        with pytest.raises(tf.ConfigurationError):
+            _lib.check(lib.tffft_comm_check(None))
+    finally:
+        for r in range(2):
+            lib.tffft_comm_destroy(arr[r])
