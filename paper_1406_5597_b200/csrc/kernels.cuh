@@ -37,7 +37,7 @@ struct ColParams {
   // (0 = off): DRAM then sees pf_bytes-wide row visits instead of B*sizeof(cx)
   long long pf_ahead;
   int pf_bytes;
-  int probe;  // profiling probes (0 = off): bit 0 skips the epilogue stores, bit 1 the prefetch loads
+  int probe;  // profiling builds only (TFFFT_PROBES=1): bit 0 skips the epilogue stores, bit 1 the prefetch loads
 };
 
 // Rows: row r of real data at real + r*n2 (reals); complex row at spec + r*n2c.
@@ -61,6 +61,11 @@ struct RowParams {
 // exchanging real and imaginary words in separate rounds, TFFFT_SPLIT=1).
 // X layout: one pad word per E words inside a column, column stride S chosen
 // so one wavefront (B columns x QW/B threads) covers every bank once.
+// profiling builds (tools/build_variants.sh ... -DTFFFT_PROBES=1): runtime probe
+// bits that skip the column kernel's loads or stores (profiles/r01s2/col_probes.txt)
+#ifndef TFFFT_PROBES
+#define TFFFT_PROBES 0
+#endif
 #ifndef TFFFT_COLB
 #define TFFFT_COLB 8
 #endif
@@ -271,13 +276,17 @@ col_fft_kernel(const ColParams prm) {
   };
   cx<T>* lo = reinterpret_cast<cx<T>*>(xs);  // [LO_E][NT] leftover slots inside the exchange buffer
   auto prefetch = [&](const Col& col) {
+#if TFFFT_PROBES
     if (prm.probe & 2) return;
+#endif
 #pragma unroll
     for (int kk = 0; kk < CF::PF_E; ++kk) cp_async<sizeof(cx<T>)>(pf + kk * NT + t, src(col, tt + TPT * kk));
     cp_commit();
   };
   auto prefetch_lo = [&](const Col& col) {
+#if TFFFT_PROBES
     if (prm.probe & 2) return;
+#endif
 #pragma unroll
     for (int kk = CF::PF_E; kk < E; ++kk)
       cp_async<sizeof(cx<T>)>(lo + (kk - CF::PF_E) * NT + t, src(col, tt + TPT * kk));
@@ -287,10 +296,6 @@ col_fft_kernel(const ColParams prm) {
   long long tile = blockIdx.x / CL;
   const long long tstep = gridDim.x / CL;
   if (tile >= ntiles) return;
-  if ((prm.probe >> 8) && (blockIdx.x & 1)) {  // probe: desynchronise odd CTAs by probe>>8 ns
-    const unsigned d = (unsigned)(prm.probe >> 8);
-    for (unsigned w = 0; w < d; w += 1000) __nanosleep(1000);
-  }
   Col cur = column(tile);
   if (CF::PREFETCH) prefetch(cur);
   if (CF::LO_E > 0) prefetch_lo(cur);
@@ -340,7 +345,10 @@ col_fft_kernel(const ColParams prm) {
       ST::finish(xs, v, tt, bl, tw);
     }
 
-    if (cur.valid && !(prm.probe & 1)) {
+#if TFFFT_PROBES
+    if (prm.probe & 1) cur.valid = false;
+#endif
+    if (cur.valid) {
       if constexpr (RD == 1) {
         const long long cofs = (long long)cur.cq * prm.stg_grp + cur.cr + prm.stg_base;
         const unsigned sw = (unsigned)prm.stg_within;

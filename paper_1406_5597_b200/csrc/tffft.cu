@@ -308,10 +308,12 @@ static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd
                               cudaStream_t s) {
   pl->launches++;
   ColParams prm = prm0;
+#if TFFFT_PROBES
   {
     static const char* probe = getenv("TFFFT_PROBE_COL");
     prm.probe = probe ? atoi(probe) : 0;
   }
+#endif
   return pl->dtype == TFFFT_F64 ? launch_col_fft<double>(L, inv, two, rd, wide, prm, s)
                                 : launch_col_fft<float>(L, inv, two, rd, wide, prm, s);
 }
@@ -402,10 +404,12 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
     c.stg_grp = (long long)pl->n1p * pl->n2c;
     c.stg_base = (long long)plane0 * c.stg_grp;
   }
+#if TFFFT_PROBES
   {  // profiling probe: every plane aliases plane 0 (same work, L2-resident footprint)
     static const char* probe = getenv("TFFFT_PROBE_ALIAS");
     if (probe && atoi(probe)) c.grp_stride = 0;
   }
+#endif
   if (rd == 0 && c.grp_stride != 0) {
     bool done = false;
     TRY(columns_tma(pl, pl->L1, inv, false, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
