@@ -108,7 +108,9 @@ __host__ __device__ constexpr int col_batch() {
   // split exchange: prefetch slots (complex) + exchange buffer (real words);
   // whole-complex exchange: the next tile's operands fit slots + exchange buffer
   constexpr size_t per_elem = TFFFT_SPLIT ? sizeof(cx<T>) + sizeof(T) : sizeof(cx<T>);
-  while (b > 1 && (TPT * b > 1024 || (size_t)b * N * per_elem + 8192 > 227 * 1024)) b /= 2;
+  // the shared-memory bound applies per CTA: a WIDE tile may span a cluster of TFFFT_COLCLUSTER CTAs
+  constexpr int cl = WIDE ? TFFFT_COLCLUSTER : 1;
+  while (b > 1 && (TPT * (b / cl) > 1024 || (size_t)(b / cl) * N * per_elem + 8192 > 227 * 1024)) b /= 2;
   return b;
 }
 template <typename T, int L, bool WIDE = false> struct ColCfg {

@@ -244,6 +244,9 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
 template <typename T, int L, bool INV, bool WIDE>
 static cudaError_t tc_one(const CUtensorMap& map, const TmaColParams& p, cudaStream_t s) {
   using TC = TmaColCfg<T, L, WIDE>;
+  if constexpr (!TC::OK) {
+    return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
+  } else {
   auto k = col_tma_kernel<T, L, INV, WIDE>;
   static cudaError_t prep = prep_smem(k, TC::SMEM);
   if (prep != cudaSuccess) return prep;
@@ -252,6 +255,7 @@ static cudaError_t tc_one(const CUtensorMap& map, const TmaColParams& p, cudaStr
   (void)cudaGetLastError();
   k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, p);
   return cudaGetLastError();
+  }
 }
 
 template <typename T, int L>
@@ -273,8 +277,10 @@ cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, const CUtenso
 template <>
 int col_tma_width<TFFFT_REAL>(int L, bool wide) {
   switch (L) {
-    case 9: return wide ? TmaColCfg<TFFFT_REAL, 9, true>::B : TmaColCfg<TFFFT_REAL, 9, false>::B;
-    case 10: return wide ? TmaColCfg<TFFFT_REAL, 10, true>::B : TmaColCfg<TFFFT_REAL, 10, false>::B;
+    case 9: return wide ? (TmaColCfg<TFFFT_REAL, 9, true>::OK ? TmaColCfg<TFFFT_REAL, 9, true>::B : 0)
+                        : (TmaColCfg<TFFFT_REAL, 9, false>::OK ? TmaColCfg<TFFFT_REAL, 9, false>::B : 0);
+    case 10: return wide ? (TmaColCfg<TFFFT_REAL, 10, true>::OK ? TmaColCfg<TFFFT_REAL, 10, true>::B : 0)
+                         : (TmaColCfg<TFFFT_REAL, 10, false>::OK ? TmaColCfg<TFFFT_REAL, 10, false>::B : 0);
     default: return 0;
   }
 }
