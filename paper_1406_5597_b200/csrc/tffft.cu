@@ -32,6 +32,7 @@
 #include "col_tma.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace tffft;
 
@@ -1267,21 +1268,34 @@ static int begin_events(tffft_plan_t pl, bool fwd, cudaStream_t s, StageEvents**
 #define MARK(ev, i, s) \
   if (ev) CUDA_TRY(cudaEventRecord((ev)->e[i], s));
 
+// NVTX ranges around each call and stage (SURVEY.md §5 tracing): header-only
+// NVTX3, a no-op unless a tool (ncu --nvtx, nsys) injects itself.
+// e.g. ncu --nvtx --nvtx-include "tffft.forward/stage3/" ...
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* stream) {
   if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
   TRY(check_ptr(real_in, "real_in", pl->esz));
   TRY(check_ptr(spec_out, "spec_out", pl->esz));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(pl->comm->device));
+  NvtxRange call("tffft.forward");
   StageEvents* ev;
   TRY(begin_events(pl, true, s, &ev));
-  // stage 1: planes (dfft.py:161-163)
-  TRY(fabric_guard_staging(pl, s));
-  if (pl->s1_fused) {
-    TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
-  } else {
-    CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
-    TRY(stage1_columns(pl, spec_out, false, s));
+  {  // stage 1: planes (dfft.py:161-163)
+    NvtxRange r("stage1");
+    TRY(fabric_guard_staging(pl, s));
+    if (pl->s1_fused) {
+      TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
+    } else {
+      CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
+      TRY(stage1_columns(pl, spec_out, false, s));
+    }
   }
   MARK(ev, 1, s);
   if (pl->strategy == 1) {
@@ -1294,12 +1308,16 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
     MARK(ev, 3, s);
     return TFFFT_OK;
   }
-  // exchange (exchange.py:263-276)
-  TRY(exchange(pl, spec_out, s));
+  {  // exchange (exchange.py:263-276)
+    NvtxRange r("exchange");
+    TRY(exchange(pl, spec_out, s));
+  }
   MARK(ev, 2, s);
-  // stage 3: strided columns (dfft.py:170-171)
-  TRY(stage3_columns(pl, spec_out, false, s));
-  TRY(fabric_landing_consumed(pl, s));
+  {  // stage 3: strided columns (dfft.py:170-171)
+    NvtxRange r("stage3");
+    TRY(stage3_columns(pl, spec_out, false, s));
+    TRY(fabric_landing_consumed(pl, s));
+  }
   MARK(ev, 3, s);
   return TFFFT_OK;
 }
@@ -1310,6 +1328,7 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
   TRY(check_ptr(real_out, "real_out", pl->esz));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(pl->comm->device));
+  NvtxRange call("tffft.inverse");
   StageEvents* ev;
   TRY(begin_events(pl, false, s, &ev));
   if (pl->s1_fused)  // the fused kernel max-reduces into the per-plane statistics
@@ -1325,19 +1344,26 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
     TRY(unpack_inverse(pl, spec, s));
     MARK(ev, 2, s);
   } else {
-    TRY(stage3_columns(pl, spec, true, s));
+    {
+      NvtxRange r("stage3");
+      TRY(stage3_columns(pl, spec, true, s));
+    }
     MARK(ev, 1, s);
-    // exchange (exchange.py:279-290)
-    TRY(exchange(pl, spec, s));
+    {  // exchange (exchange.py:279-290)
+      NvtxRange r("exchange");
+      TRY(exchange(pl, spec, s));
+    }
     MARK(ev, 2, s);
   }
-  // stage 1' (dfft.py:206-209)
-  if (pl->s1_fused) {
-    TRY(stage1_fused(pl, real_out, spec, false, s));
-  } else {
-    TRY(stage1_columns(pl, spec, true, s));
-    TRY(fabric_landing_consumed(pl, s));
-    CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+  {  // stage 1' (dfft.py:206-209)
+    NvtxRange r("stage1");
+    if (pl->s1_fused) {
+      TRY(stage1_fused(pl, real_out, spec, false, s));
+    } else {
+      TRY(stage1_columns(pl, spec, true, s));
+      TRY(fabric_landing_consumed(pl, s));
+      CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+    }
   }
   MARK(ev, 3, s);
   pl->last_inverse_stream = s;
