@@ -11,3 +11,8 @@ for extra in "--dtype float32" "--grid 512" "--config turbulence --steps 5"; do
   timeout 600 python bench.py --no-cpu $extra >> $OUT/bench_lines.json 2>> $OUT/bench_lines.err
 done
 timeout 900 bash tools/profile_round.sh ${1:-r}/prof
+for extra in "--dtype float32" "--grid 512"; do
+  tag=$(echo $extra | tr -d ' -')
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file gpurun_out/${1:-r}/prof/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 $extra > /dev/null 2>&1
+done
