@@ -42,11 +42,13 @@ struct TmaColCfg {
   static constexpr int NPF = NBOX > 1 ? NBOX / 2 : 1;  // boxes landing in the prefetch region
   static constexpr size_t BOXB = sizeof(cx<T>) * (size_t)BOX * B;
   static constexpr size_t PF = BOXB * NPF;
-  static constexpr size_t X = CF::X_BYTES > BOXB * (NBOX - NPF) ? CF::X_BYTES : BOXB * (NBOX - NPF);
+  // the odd-row boxes of the parity mode are two complex wider (pitch B + 2)
+  static constexpr size_t XB = sizeof(cx<T>) * (size_t)BOX * (B + 2) * (NBOX - NPF);
+  static constexpr size_t X = CF::X_BYTES > XB ? CF::X_BYTES : XB;
   static constexpr int TW = SH::TW > 0 ? SH::TW : 1;
   static constexpr size_t SMEM = PF + X + sizeof(cx<T>) * TW + 64;
   static constexpr bool OK = CF::CL == 1 && CF::GROUPS == 1 && CF::XCHG && SMEM <= 227 * 1024 &&
-                             B * sizeof(cx<T>) <= 256;
+                             B * sizeof(cx<T>) <= 256 && (NBOX == 1 || 2 * NPF == NBOX) && SH::TPT % 2 == 0;
 };
 
 struct TmaColParams {
@@ -58,11 +60,15 @@ struct TmaColParams {
   long long rstride;     // elements between the rows of a column
   long long gstride;     // elements between groups
   int evict_first;       // L2 priority of the loads: 1 evict_first, 0 evict_normal (rows not 128-byte aligned)
+  int parity;            // rows 8 bytes off 16-byte alignment on odd rows: even rows through `map`, odd
+                         // rows through `map_odd`, whose boxes start on the aligned address before the
+                         // row segment and are one complex wider on each side (pitch B + 2, data at +1)
 };
 
 template <typename T, int L, bool INV, bool WIDE>
 __global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, 1)
-col_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaColParams prm) {
+col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_odd,
+               const TmaColParams prm) {
   using TC = TmaColCfg<T, L, WIDE>;
   using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
@@ -100,19 +106,28 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaColParams prm) 
     c0 = (int)(tile % prm.tpg) * B;
   };
   // half h of tile i: boxes [0, NPF) into the prefetch region, the rest into the exchange buffer
+  // Parity mode: half 0 = the even rows (map, row index r/2), half 1 = the odd
+  // rows (map_odd); a thread's operand rows tt + TPT kk all share tt's parity.
   auto load_half = [&](long long i, int h) {
     int grp, c0;
     coords(i, grp, c0);
     const int q0 = h ? TC::NPF : 0, q1 = h ? TC::NBOX : TC::NPF;
     if (q1 <= q0) return;
     fence_async_shared();  // the CTA's generic accesses to the region are ordered before the TMA writes
-    mbar_arrive_tx(bar + h, (unsigned)(TC::BOXB * (q1 - q0)));
+    const int pitch = (prm.parity && h) ? B + 2 : B;
+    mbar_arrive_tx(bar + h, (unsigned)(sizeof(cx<T>) * (size_t)BOX * pitch * (q1 - q0)));
     cx<T>* dst = h ? xb : pf;
-    for (int q = q0; q < q1; ++q)
-      tma_load3(dst + (size_t)(q - q0) * BOX * B, &map, 2 * c0, q * BOX, grp, bar + h, pol);
+    for (int q = q0; q < q1; ++q) {
+      if (prm.parity)
+        tma_load3(dst + (size_t)(q - q0) * BOX * pitch, h ? &map_odd : &map, 2 * c0, (q - q0) * BOX, grp, bar + h,
+                  pol);
+      else
+        tma_load3(dst + (size_t)(q - q0) * BOX * B, &map, 2 * c0, q * BOX, grp, bar + h, pol);
+    }
   };
   auto operand = [&](int kk) -> cx<T> {  // row tt + TPT kk; kk is a compile-time constant after unrolling
     const int r = tt + TPT * kk;
+    if (prm.parity) return (tt & 1) ? xb[(r >> 1) * (B + 2) + 1 + b] : pf[(r >> 1) * B + b];
     return (TPT * kk) / BOX < TC::NPF ? pf[r * B + b] : xb[(r - TC::NPF * BOX) * B + b];
   };
 
@@ -151,7 +166,8 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const TmaColParams prm) 
 __host__ __device__ constexpr bool col_tma_supported(int L) { return L == 9 || L == 10; }
 
 template <typename T>
-cudaError_t launch_col_tma(int L, bool inv, bool wide, const CUtensorMap& map, const TmaColParams& p, cudaStream_t s);
+cudaError_t launch_col_tma(int L, bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+                           const TmaColParams& p, cudaStream_t s);
 // columns per tile (the box width) of the TMA column kernel
 template <typename T>
 int col_tma_width(int L, bool wide);

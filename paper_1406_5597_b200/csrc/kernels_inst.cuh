@@ -242,7 +242,7 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
 }
 
 template <typename T, int L, bool INV, bool WIDE>
-static cudaError_t tc_one(const CUtensorMap& map, const TmaColParams& p, cudaStream_t s) {
+static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, const TmaColParams& p, cudaStream_t s) {
   using TC = TmaColCfg<T, L, WIDE>;
   if constexpr (!TC::OK) {
     return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
@@ -253,23 +253,24 @@ static cudaError_t tc_one(const CUtensorMap& map, const TmaColParams& p, cudaStr
   if (p.ntiles <= 0) return cudaSuccess;
   const long long blocks = std::min<long long>(p.ntiles, num_sms());
   (void)cudaGetLastError();
-  k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, p);
+  k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, map_odd, p);
   return cudaGetLastError();
   }
 }
 
 template <typename T, int L>
-static cudaError_t tc_dispatch(bool inv, bool wide, const CUtensorMap& map, const TmaColParams& p, cudaStream_t s) {
-  if (wide) return inv ? tc_one<T, L, true, true>(map, p, s) : tc_one<T, L, false, true>(map, p, s);
-  return inv ? tc_one<T, L, true, false>(map, p, s) : tc_one<T, L, false, false>(map, p, s);
+static cudaError_t tc_dispatch(bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+                               const TmaColParams& p, cudaStream_t s) {
+  if (wide) return inv ? tc_one<T, L, true, true>(map, map_odd, p, s) : tc_one<T, L, false, true>(map, map_odd, p, s);
+  return inv ? tc_one<T, L, true, false>(map, map_odd, p, s) : tc_one<T, L, false, false>(map, map_odd, p, s);
 }
 
 template <>
-cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, const CUtensorMap& map, const TmaColParams& p,
-                                       cudaStream_t s) {
+cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+                                       const TmaColParams& p, cudaStream_t s) {
   switch (L) {
-    case 9: return tc_dispatch<TFFFT_REAL, 9>(inv, wide, map, p, s);
-    case 10: return tc_dispatch<TFFFT_REAL, 10>(inv, wide, map, p, s);
+    case 9: return tc_dispatch<TFFFT_REAL, 9>(inv, wide, map, map_odd, p, s);
+    case 10: return tc_dispatch<TFFFT_REAL, 10>(inv, wide, map, map_odd, p, s);
     default: return cudaErrorInvalidValue;
   }
 }

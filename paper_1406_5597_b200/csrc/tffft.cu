@@ -413,7 +413,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
 #endif
   if (rd == 0 && c.grp_stride != 0) {
     bool done = false;
-    TRY(columns_tma(pl, pl->L1, inv, false, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
+    TRY(columns_tma(pl, pl->L1, inv, true, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
                     pl->tw1, s, &done));
     if (done) return TFFFT_OK;
   }
@@ -463,17 +463,38 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
   *done = false;
   const long long esz = (long long)pl->esz;
-  if (!tma_cols_enabled(pl, wide) || !col_tma_supported(L) || (rstride * esz) % 16 || (ngrp > 1 && (gstride * esz) % 16) ||
-      reinterpret_cast<uintptr_t>(base) % 16)
+  const long long rbytes = rstride * esz;
+  // rows 16-byte aligned (one map), or 8 bytes off on odd rows only (float32
+  // stage 1b, n2c odd: 4104-byte rows): even and odd rows through two maps
+  const bool parity = rbytes % 16 != 0;
+  if (!tma_cols_enabled(pl, wide) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
+      (ngrp > 1 && (gstride * esz) % 16) || reinterpret_cast<uintptr_t>(base) % 16)
     return TFFFT_OK;
   const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
   if (B <= 0) return TFFFT_OK;
-  CUtensorMap map;
+  CUtensorMap map, map_odd;
   const long long n = 1LL << L;
-  cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
-  cuuint64_t st[2] = {(cuuint64_t)(rstride * esz), (cuuint64_t)(ngrp > 1 ? gstride * esz : n * rstride * esz)};
-  cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n, 256), 1};
-  TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+  const long long gbytes = ngrp > 1 ? gstride * esz : n * rbytes;
+  if (!parity) {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
+    cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n, 256), 1};
+    TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+    map_odd = map;
+  } else {
+    // odd rows miss 16-byte alignment by `mis` = one complex: their boxes start
+    // one complex early (aligned) and are two complex wider (pitch B + 2)
+    const long long mis = rbytes % 16;
+    if (mis != esz) return TFFFT_OK;
+    cuuint64_t de[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)(n / 2), (cuuint64_t)ngrp};
+    cuuint64_t dodd[3] = {(cuuint64_t)(2 * cols + 2), (cuuint64_t)(n / 2), (cuuint64_t)ngrp};
+    cuuint64_t st[2] = {(cuuint64_t)(2 * rbytes), (cuuint64_t)gbytes};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n / 2, 256), 1};
+    cuuint32_t boxo[3] = {(cuuint32_t)(2 * B + 4), (cuuint32_t)std::min<long long>(n / 2, 256), 1};
+    TRY(make_map(pl, &map, base, 3, de, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+    TRY(make_map(pl, &map_odd, static_cast<char*>(base) + rbytes - mis, 3, dodd, st, boxo,
+                 CU_TENSOR_MAP_L2_PROMOTION_NONE));
+  }
   TmaColParams w{};
   w.data = base;
   w.tw = tw;
@@ -482,13 +503,14 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   w.cols = (int)cols;
   w.rstride = rstride;
   w.gstride = gstride;
+  w.parity = parity;
   {
     static const char* ef = getenv("TFFFT_TMA_EF");
-    w.evict_first = ef ? atoi(ef) : ((rstride * esz) % 128 == 0);
+    w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
   }
   pl->launches++;
-  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, map, w, s)
-                                               : launch_col_tma<float>(L, inv, wide, map, w, s);
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, map, map_odd, w, s)
+                                               : launch_col_tma<float>(L, inv, wide, map, map_odd, w, s);
   CUDA_TRY(e);
   *done = true;
   return TFFFT_OK;
