@@ -93,7 +93,7 @@ enum {
                                      exchange reduces to a barrier.  Local fabric communicators. */
   TFFFT_FLAG_TMA_COLUMNS = 16     /* p = 1 column passes of length 512 / 1024 fed by TMA box copies
                                      (col_ws.cuh) wherever the row stride allows; without flags
-                                     (flags < 0) only the measured winner, float32 stage 3, uses them */
+                                     (flags < 0) only the measured winner, float32 (stages 1b and 3), uses them */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

@@ -233,7 +233,7 @@ struct tffft_plan_s {
   // fused stage 1 (stage1_fused.cuh)
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
-  int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 stage 3 only
+  int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 only (stages 1b and 3)
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -456,8 +456,8 @@ static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const
 // of `cols` contiguous columns, column elements `rstride` apart, groups
 // `gstride` apart (elements).  Sets *done = false when the shape has no TMA
 // path (the caller falls back to col_fft_kernel).
-static bool tma_cols_enabled(tffft_plan_t pl, bool wide) {
-  return pl->tma_cols == 1 || (pl->tma_cols == 2 && wide && pl->dtype == TFFFT_F32);
+static bool tma_cols_enabled(tffft_plan_t pl) {
+  return pl->tma_cols == 1 || (pl->tma_cols == 2 && pl->dtype == TFFFT_F32);
 }
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
@@ -467,7 +467,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   // rows 16-byte aligned (one map), or 8 bytes off on odd rows only (float32
   // stage 1b, n2c odd: 4104-byte rows): even and odd rows through two maps
   const bool parity = rbytes % 16 != 0;
-  if (!tma_cols_enabled(pl, wide) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
+  if (!tma_cols_enabled(pl) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
       (ngrp > 1 && (gstride * esz) % 16) || reinterpret_cast<uintptr_t>(base) % 16)
     return TFFFT_OK;
   const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
@@ -1114,7 +1114,7 @@ int tffft_plan_attach_peers(tffft_plan_t pl, const uint8_t* handles) {
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* out) {
   // TMA column passes: explicit flag = every supported pass; environment
-  // defaults = the measured winner (float32 stage 3, profiles/r01s2/tma_cols.txt)
+  // defaults = the measured winner (float32 column passes, profiles/r01s2/tma_cols.txt, r01s6/f32_stage1b_tma.txt)
   // unless TFFFT_TMA_COLS says otherwise
   int tma_cols = 0;
   if (flags < 0) {
