@@ -373,7 +373,9 @@ def run_gpu(args):
                                   "stage3+3'": st3_ms * 2},
             "roundtrip_rel_l2": rt,
         },
-        "roofline": {"bound": "hbm", "kernel": "col_fft_kernel (stage 3 strided n0 c2c)",
+        "roofline": {"bound": "hbm",
+                     "kernel": (("col_tma_kernel" if dt == "float32" and p == 1 else "col_fft_kernel")
+                                + " (stage 3 strided n0 c2c)"),
                      "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": st3},
