@@ -160,10 +160,10 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #define TFFFT_ROW_MINB 1
 #endif
 #ifndef TFFFT_C2R_MINB9
-#define TFFFT_C2R_MINB9 6
+#define TFFFT_C2R_MINB9 5
 #endif
 #ifndef TFFFT_R2C_MINB9
-#define TFFFT_R2C_MINB9 6
+#define TFFFT_R2C_MINB9 8
 #endif
 // r2c row schedule: float64 rows of n2 = 1024 run the radix-8 schedule
 // (3 passes, E = 8, 6 CTAs/SM: 3.10 ms per 1024^3 launch vs 3.62 ms with radix
@@ -190,11 +190,11 @@ template <int L, int MB = 0> struct RowCfg {
   static constexpr int PS = Shape<L, MB>::EB > 0 ? Shape<L, MB>::EB : 30;  // one pad slot per E elements
   static constexpr int N = Shape<L, MB>::N;
   static constexpr int S = N + (N >> (PS > 20 ? 30 : PS)) + 1 + 1;   // room for bin N in c2r
-  // n2 = 1024 row kernels: r2c would take 93 and c2r (with its consistency
-  // statistics) 111 registers, i.e. 5 / 4 CTAs of 128 threads per SM; asking
-  // for 6 CTAs caps both at 80 registers with no spills (measured best of 5 / 6
-  // / 8: c2r 3.54 -> 3.47 ms, r2c 3.17 -> 3.10 ms per 1024^3 launch).  Other
-  // lengths spill under such caps and keep the default.
+  // n2 = 1024 float64 row kernels on the radix-8 schedule: occupancy by
+  // launch bounds, measured over 5 / 6 / 7 / 8 CTAs of 128 threads per SM
+  // (profiles/r01s7/row_minb.txt): r2c best at 8 (64 registers, no spills,
+  // 2.69 ms per 1024^3 launch), c2r -- with its consistency statistics and
+  // pair loads -- at 5 (94 registers, 2.88 ms).  Other lengths keep the default.
   // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
   static constexpr bool CAP = L == 9 && THREADS == 128 && Shape<L, MB>::E == 8;
   static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
