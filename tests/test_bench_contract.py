@@ -1,0 +1,48 @@
+"""bench.py's JSON contract (the driver parses one line per run).  The
+reference arm runs on the CPU here; the GPU arm runs on the B200 box."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout=600):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True, text=True,
+                         timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    """--impl reference: the oracle port timed on the host cores, same metric
+    and unit as the GPU arm, plus cpu_baseline and a zero-copy e2e."""
+    d = _run(["--impl", "reference", "--grid", "32", "--steps", "1", "--warmup", "0", "--cpu-planes", "8"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["unit"] == "GFLOP/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line():
+    """The GPU arm at a small grid: device-timed value, roofline with the
+    stage-3 kernel, host-buffer e2e, launch count, clocks, cpu_baseline."""
+    d = _run(["--grid", "128", "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--cpu-planes", "8"])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"]["roundtrip_rel_l2"] <= 1e-12
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] < 1.5 and r["unit"] == "GB/s"
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] == 128 ** 3 * 8 and e["d2h_bytes_per_step"] == 128 ** 3 * 8
+    assert d["gpu_launches"] == 6 * 3  # six kernels per forward + inverse pair
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["cpu_baseline"]["value"] > 0
