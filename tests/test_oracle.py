@@ -139,3 +139,65 @@ def test_strided_offsets_match_spectral_offset():
     for c in range(offs.shape[0]):
         j, k = divmod(c, n2c)
         assert list(offs[c]) == [oracle.spectral_offset(n0, n1, n2, p, j, r, k) for r in range(n0)]
+
+
+# --- further restatements of pkg/tests/test_kernels.py --------------------
+
+def test_c2c_linearity():
+    """TestC2C linearity (test_kernels.py:53-113)."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    y = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    a, b = 2.5 - 1j, -0.75 + 0.5j
+    np.testing.assert_allclose(c2c(a * x + b * y), a * c2c(x) + b * c2c(y), atol=1e-12)
+
+
+def test_r2c_edge_bins_real_and_hermitian_embedding():
+    """TestRealTransforms (test_kernels.py:179-234): the DC and Nyquist bins of
+    a real row are real, and r2c equals the first n/2+1 bins of the full c2c."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((3, 16))
+    half = oracle.r2c_rows(x)
+    assert half.shape == (3, 9)
+    assert np.all(half[:, 0].imag == 0) and np.max(np.abs(half[:, 8].imag)) <= 1e-14
+    full = x.astype(np.complex128)
+    oracle.c2c_rows(full, False)
+    np.testing.assert_allclose(half, full[:, :9], atol=1e-13)
+
+
+def test_real_round_trip_is_unnormalised():
+    """c2r(r2c(x)) = n x (test_kernels.py: unnormalised round trip, 8 x at n = 8)."""
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2, 8))
+    back, _ = oracle.c2r_rows(oracle.r2c_rows(x), 8)
+    np.testing.assert_allclose(back, 8 * x, atol=1e-12)
+
+
+def test_plane_transform_vs_naive_2d():
+    """TestPlaneTransforms (test_kernels.py:237-268): a 4 x 4 plane r2c
+    against a naive 2D DFT, and the plane round trip x n1 n2."""
+    rng = np.random.default_rng(13)
+    plane = rng.standard_normal((1, 4, 4))
+    got = oracle.stage1_forward(plane)
+    want = np.stack([oracle.dft1d_naive(col) for col in
+                     np.stack([oracle.dft1d_naive(r)[:3] for r in plane[0]]).T]).T
+    assert np.max(np.abs(got.reshape(4, 3) - want)) <= 1e-12
+    back, _ = oracle.stage1_inverse(got.copy(), 4)
+    np.testing.assert_allclose(back.reshape(4, 4), 16 * plane[0], atol=1e-12)
+
+
+def test_stage3_equals_gather_fft_scatter():
+    """TestC2CStrided (test_kernels.py:141-158): the strided column FFT is
+    bitwise the gather -> FFT -> scatter of the same column."""
+    n0, n1, n2, p = 8, 4, 4, 2
+    rng = np.random.default_rng(17)
+    n2c = n2 // 2 + 1
+    flat = rng.standard_normal((n1 // p) * n0 * n2c) + 1j * rng.standard_normal((n1 // p) * n0 * n2c)
+    offs = oracle.strided_column_offsets(n0, n1, n2, p)
+    want = flat.copy()
+    cols = want[offs].copy()
+    oracle.c2c_rows(cols, False)
+    want[offs] = cols
+    got = flat.copy()
+    oracle.stage3(got, n0, n1, n2, p, inverse=False)
+    assert np.array_equal(got.view(np.float64), want.view(np.float64))
