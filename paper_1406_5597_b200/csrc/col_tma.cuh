@@ -60,6 +60,7 @@ struct TmaColParams {
   long long rstride;     // elements between the rows of a column
   long long gstride;     // elements between groups
   int evict_first;       // L2 priority of the loads: 1 evict_first, 0 evict_normal (rows not 128-byte aligned)
+  unsigned long long* ticket;  // dynamic tile order (zeroed before the launch), or null: round robin
   int parity;            // rows 8 bytes off 16-byte alignment on odd rows: even rows through `map`, odd
                          // rows through `map_odd`, whose boxes start on the aligned address before the
                          // row segment and are one complex wider on each side (pitch B + 2, data at +1)
@@ -97,20 +98,33 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
   }
   __syncthreads();
 
-  const long long first = blockIdx.x, step = gridDim.x;
-  const long long mine = prm.ntiles > first ? (prm.ntiles - 1 - first) / step + 1 : 0;
+  const long long step = gridDim.x;
   const uint64_t pol = prm.evict_first ? policy_evict_first() : policy_evict_normal();
-  auto coords = [&](long long i, int& grp, int& c0) {
-    const long long tile = first + i * step;
+  auto coords = [&](long long tile, int& grp, int& c0) {
     grp = (int)(tile / prm.tpg);
     c0 = (int)(tile % prm.tpg) * B;
   };
+  // tile order: a ticket counter keeps the tiles in flight within a window of
+  // ~gridDim consecutive tiles (DRAM page locality of neighbours, as in
+  // col_fft_kernel); round robin without one
+  const bool dyn = prm.ticket != nullptr;
+  __shared__ long long s_tk[2];
+  long long cur = blockIdx.x;
+  if (dyn) {
+    if (t == 0) {
+      cur = (long long)atomicAdd(prm.ticket, 1ull);
+      s_tk[0] = (long long)atomicAdd(prm.ticket, 1ull);
+      s_tk[1] = cur;
+    }
+    __syncthreads();
+    cur = s_tk[1];
+  }
   // half h of tile i: boxes [0, NPF) into the prefetch region, the rest into the exchange buffer
   // Parity mode: half 0 = the even rows (map, row index r/2), half 1 = the odd
   // rows (map_odd); a thread's operand rows tt + TPT kk all share tt's parity.
-  auto load_half = [&](long long i, int h) {
+  auto load_half = [&](long long tile, int h) {
     int grp, c0;
-    coords(i, grp, c0);
+    coords(tile, grp, c0);
     const int q0 = h ? TC::NPF : 0, q1 = h ? TC::NBOX : TC::NPF;
     if (q1 <= q0) return;
     fence_async_shared();  // the CTA's generic accesses to the region are ordered before the TMA writes
@@ -131,11 +145,12 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     return (TPT * kk) / BOX < TC::NPF ? pf[r * B + b] : xb[(r - TC::NPF * BOX) * B + b];
   };
 
-  if (t == 0 && mine > 0) {
-    load_half(0, 0);
-    load_half(0, 1);
+  if (t == 0 && cur < prm.ntiles) {
+    load_half(cur, 0);
+    load_half(cur, 1);
   }
-  for (long long i = 0; i < mine; ++i) {
+  for (long long i = 0; cur < prm.ntiles; ++i) {
+    const long long nxt = dyn ? s_tk[i & 1] : cur + step;
     const unsigned par = (unsigned)(i & 1);
     mbar_wait(bar + 0, par);
     if (TC::NBOX > TC::NPF) mbar_wait(bar + 1, par);
@@ -143,14 +158,17 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
 #pragma unroll
     for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = operand(kk);
     __syncthreads();  // every operand read: both halves may be overwritten
-    if (t == 0 && i + 1 < mine) load_half(i + 1, 0);
+    if (t == 0) {
+      if (dyn) s_tk[(i + 1) & 1] = (long long)atomicAdd(prm.ticket, 1ull);  // read next iteration, after the exchange barriers
+      if (nxt < prm.ntiles) load_half(nxt, 0);
+    }
     ST::first(v, tt, s_tw);
     auto hook = [&] {  // the last exchange has drained the buffer
-      if (t == 0 && i + 1 < mine) load_half(i + 1, 1);
+      if (t == 0 && nxt < prm.ntiles) load_half(nxt, 1);
     };
     ST::finish(xs, v, tt, b, s_tw, hook);
     int grp, c0;
-    coords(i, grp, c0);
+    coords(cur, grp, c0);
     if (c0 + b < prm.cols) {
       cx<T>* col = reinterpret_cast<cx<T>*>(prm.data) + (long long)grp * prm.gstride + (c0 + b);
       const unsigned rs = (unsigned)prm.rstride;
@@ -159,6 +177,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
 #pragma unroll
         for (int m = 0; m < SH::RL; ++m) col[(unsigned)SH::out_elem(tt, u, m) * rs] = v[u * SH::RL + m];
     }
+    cur = nxt;
   }
 }
 

@@ -233,6 +233,7 @@ struct tffft_plan_s {
   // fused stage 1 (stage1_fused.cuh)
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
+  unsigned long long* col_ticket = nullptr;  // dynamic tile counter of the column kernel (TFFFT_COL_TICKET)
   int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 only (stages 1b and 3)
   size_t workspace = 0;
   bool timing = false;
@@ -309,6 +310,10 @@ static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd
                               cudaStream_t s) {
   pl->launches++;
   ColParams prm = prm0;
+  if (TFFFT_COL_TICKET) {
+    prm.ticket = pl->col_ticket;
+    (void)cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s);
+  }
 #if TFFFT_PROBES
   {
     static const char* probe = getenv("TFFFT_PROBE_COL");
@@ -504,6 +509,10 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   w.rstride = rstride;
   w.gstride = gstride;
   w.parity = parity;
+  if (TFFFT_COL_TICKET) {
+    w.ticket = pl->col_ticket;
+    CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
+  }
   {
     static const char* ef = getenv("TFFFT_TMA_EF");
     w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
@@ -1163,6 +1172,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   TRY(upload_table(pass_table(pl->L2h, r2c_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2r, &ws));
   TRY(upload_table(pass_table(pl->L2h, c2r_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2c, &ws));
   TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
+  CUDA_TRY(cudaMalloc(&pl->col_ticket, sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
   CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
   ws += sizeof(unsigned long long) * 3 * pl->n0p;
@@ -1261,6 +1271,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
+  cudaFree(pl->col_ticket);
   for (size_t q = 0; q < pl->peer_landing.size(); ++q)
     if (pl->peer_landing[q] && (int)q != pl->rank) cudaIpcCloseMemHandle(pl->peer_landing[q]);
   cudaFree(pl->barrier_word);
