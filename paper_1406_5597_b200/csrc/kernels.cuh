@@ -306,10 +306,12 @@ col_fft_kernel(const ColParams prm) {
   // the CTAs drift apart, so neighbouring tiles -- the rest of the same DRAM
   // pages -- are fetched together (1024^3 f64 stage 3: 3.68 -> 3.25 ms).
   // Needs the CTA barriers of the exchange in every iteration (P > 1).
-  constexpr bool DYN = TFFFT_COL_TICKET && CF::XCHG && CL == 1;
+  // (the host passes a counter only where it was measured faster: columns of 1024+)
+  constexpr bool DYN_OK = TFFFT_COL_TICKET && CF::XCHG && CL == 1;
+  const bool dyn = DYN_OK && prm.ticket != nullptr;
   __shared__ long long s_tk[2];
   long long it = 0;
-  if constexpr (DYN) {
+  if (dyn) {
     if (t == 0) {
       tile = (long long)atomicAdd(prm.ticket, 1ull);
       s_tk[0] = (long long)atomicAdd(prm.ticket, 1ull);
@@ -324,7 +326,7 @@ col_fft_kernel(const ColParams prm) {
   if (CF::LO_E > 0) prefetch_lo(cur);
   // tiles sharing one pf_bytes-wide row segment; each prefetches N/GT rows
   const int GT = prm.pf_ahead > 0 ? prm.pf_bytes / (B * (int)sizeof(cx<T>)) : 1;
-  for (; tile < ntiles; tile = DYN ? tile : tile + tstep) {
+  for (; tile < ntiles; tile = dyn ? tile : tile + tstep) {
     if constexpr (CL > 1 && TFFFT_COLCLUSTER_SYNC) {
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
     }
@@ -343,7 +345,7 @@ col_fft_kernel(const ColParams prm) {
     cx<T> v[E];
     Col next = cur;
     long long nxt = tile + tstep;
-    if constexpr (DYN) {
+    if (dyn) {
       nxt = s_tk[it & 1];
       if (t == 0) s_tk[(it + 1) & 1] = (long long)atomicAdd(prm.ticket, 1ull);  // read next iteration, after the barriers below
       ++it;
@@ -402,7 +404,7 @@ col_fft_kernel(const ColParams prm) {
       }
     }
     cur = next;
-    if constexpr (DYN) tile = nxt;
+    if (dyn) tile = nxt;
   }
 }
 

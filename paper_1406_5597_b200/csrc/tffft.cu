@@ -310,7 +310,9 @@ static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd
                               cudaStream_t s) {
   pl->launches++;
   ColParams prm = prm0;
-  if (TFFFT_COL_TICKET) {
+  // dynamic tile order for columns of 1024 and longer (1024^3 f64 stage 3
+  // 3.69 -> 3.25 ms); 512-point columns measured 5% slower with it
+  if (TFFFT_COL_TICKET && L >= 10) {
     prm.ticket = pl->col_ticket;
     (void)cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s);
   }
@@ -509,7 +511,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   w.rstride = rstride;
   w.gstride = gstride;
   w.parity = parity;
-  if (TFFFT_COL_TICKET) {
+  if (TFFFT_COL_TICKET && L >= 10) {
     w.ticket = pl->col_ticket;
     CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
   }
