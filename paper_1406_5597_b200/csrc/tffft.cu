@@ -234,7 +234,7 @@ struct tffft_plan_s {
   bool s1_fused = false;
   unsigned* s1_counters = nullptr;
   unsigned long long* col_ticket = nullptr;  // dynamic tile counter of the column kernel (TFFFT_COL_TICKET)
-  int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 float32 only (stages 1b and 3)
+  int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 the measured winners
   size_t workspace = 0;
   bool timing = false;
   std::vector<StageEvents> events;
@@ -463,8 +463,11 @@ static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const
 // of `cols` contiguous columns, column elements `rstride` apart, groups
 // `gstride` apart (elements).  Sets *done = false when the shape has no TMA
 // path (the caller falls back to col_fft_kernel).
-static bool tma_cols_enabled(tffft_plan_t pl) {
-  return pl->tma_cols == 1 || (pl->tma_cols == 2 && pl->dtype == TFFFT_F32);
+// auto mode (tma_cols == 2): the measured winners -- float32 column passes,
+// and float64 columns of 1024 (with the ticket order: 3.3-3.5 -> 2.96 ms per
+// 1024^3 launch, profiles/r01s10/tma_f64_ticket.txt)
+static bool tma_cols_enabled(tffft_plan_t pl, int L) {
+  return pl->tma_cols == 1 || (pl->tma_cols == 2 && (pl->dtype == TFFFT_F32 || L >= 10));
 }
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
@@ -474,7 +477,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   // rows 16-byte aligned (one map), or 8 bytes off on odd rows only (float32
   // stage 1b, n2c odd: 4104-byte rows): even and odd rows through two maps
   const bool parity = rbytes % 16 != 0;
-  if (!tma_cols_enabled(pl) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
+  if (!tma_cols_enabled(pl, L) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
       (ngrp > 1 && (gstride * esz) % 16) || reinterpret_cast<uintptr_t>(base) % 16)
     return TFFFT_OK;
   const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
