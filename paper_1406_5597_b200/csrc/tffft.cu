@@ -306,13 +306,23 @@ static int upload_table(const std::vector<double>& t, int dtype, void** dev, siz
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 // ---------------------------------------------------------------------------
+// shortest column (log2) that takes the ticket tile order: measured gains for
+// the cp.async column kernel from 1024 points (512: 5% slower), for the TMA
+// column kernel from 512 points (profiles/r01s11/tma_512.txt)
+static int ticket_min_log(bool tma) {
+  static const int v = [] {
+    const char* e = getenv("TFFFT_TICKET_MINL");
+    return e ? atoi(e) : 0;
+  }();
+  return v > 0 ? v : (tma ? 9 : 10);
+}
+
 static cudaError_t col_launch(tffft_plan_t pl, int L, bool inv, bool two, int rd, bool wide, const ColParams& prm0,
                               cudaStream_t s) {
   pl->launches++;
   ColParams prm = prm0;
-  // dynamic tile order for columns of 1024 and longer (1024^3 f64 stage 3
-  // 3.69 -> 3.25 ms); 512-point columns measured 5% slower with it
-  if (TFFFT_COL_TICKET && L >= 10) {
+  // dynamic tile order (1024^3 f64 stage 3 3.69 -> 3.25 ms)
+  if (TFFFT_COL_TICKET && L >= ticket_min_log(false)) {
     prm.ticket = pl->col_ticket;
     (void)cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s);
   }
@@ -463,12 +473,14 @@ static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const
 // of `cols` contiguous columns, column elements `rstride` apart, groups
 // `gstride` apart (elements).  Sets *done = false when the shape has no TMA
 // path (the caller falls back to col_fft_kernel).
-// auto mode (tma_cols == 2): the measured winners -- float32 column passes,
-// and float64 columns of 1024 (with the ticket order: 3.3-3.5 -> 2.96 ms per
-// 1024^3 launch, profiles/r01s10/tma_f64_ticket.txt)
+// auto mode (tma_cols == 2): every supported column pass -- measured faster
+// than the cp.async kernel for both precisions at 512 and 1024 points
+// (profiles/r01s10/tma_f64_ticket.txt, r01s11/tma_512.txt)
 static bool tma_cols_enabled(tffft_plan_t pl, int L) {
-  return pl->tma_cols == 1 || (pl->tma_cols == 2 && (pl->dtype == TFFFT_F32 || L >= 10));
+  (void)L;
+  return pl->tma_cols != 0;
 }
+
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
   *done = false;
@@ -514,7 +526,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   w.rstride = rstride;
   w.gstride = gstride;
   w.parity = parity;
-  if (TFFFT_COL_TICKET && L >= 10) {
+  if (TFFFT_COL_TICKET && L >= ticket_min_log(true)) {
     w.ticket = pl->col_ticket;
     CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
   }
