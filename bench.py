@@ -374,8 +374,8 @@ def run_gpu(args):
             "roundtrip_rel_l2": rt,
         },
         "roofline": {"bound": "hbm",
-                     "kernel": (("col_tma_kernel" if p == 1 and (n0 == 1024 or (dt == "float32" and n0 == 512))
-                                 else "col_fft_kernel") + " (stage 3 strided n0 c2c)"),
+                     "kernel": (("col_tma_kernel" if p == 1 and n0 in (512, 1024) else "col_fft_kernel")
+                                + " (stage 3 strided n0 c2c)"),
                      "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": st3},

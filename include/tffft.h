@@ -92,8 +92,8 @@ enum {
                                      straight into the peer's landing buffer (peer memory), and the
                                      exchange reduces to a barrier.  Local fabric communicators. */
   TFFFT_FLAG_TMA_COLUMNS = 16     /* p = 1 column passes of length 512 / 1024 fed by TMA box copies
-                                     (col_ws.cuh) wherever the row stride allows; without flags
-                                     (flags < 0) only the measured winner, float32 (stages 1b and 3), uses them */
+                                     (col_tma.cuh), the default (flags < 0) unless TFFFT_TMA_COLS=0;
+                                     explicit flags without it select the cp.async column kernel */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

@@ -134,7 +134,8 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     ``algorithms`` selects optional kernel schedules ("fused_stage1",
     "fourstep_stage3", "peer_stores", "tma_columns"); None takes the library
     defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS environment
-    switches; by default the float32 column passes at p = 1 are TMA-fed)."""
+    switches; by default the 512- and 1024-point column passes at p = 1 are
+    TMA-fed)."""
     validate(grid, comm.p)
     if not isinstance(comm_pattern, CommPattern):
         raise ConfigurationError(f"comm_pattern must be a CommPattern, got {comm_pattern!r}")
