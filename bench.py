@@ -239,7 +239,9 @@ def run_gpu(args):
     grid = tf.GlobalGrid(n0, n1, n2)
     dt = args.dtype
     s_r = 8 if dt == "float64" else 4
-    fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dt, check_consistency=False)
+    # the reference's inverse checks the half spectrum on every call
+    # (kernels.py:223-238): so does the timed pair (reduction + host check)
+    fp = tf.plan(grid, ep, tf.Strategy.STRIDED, dtype=dt, check_consistency=True)
     rdt = tf.DTYPES[dt][1]
     n0p = n0 // p
     gen = torch.Generator(device=dev)

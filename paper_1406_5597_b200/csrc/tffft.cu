@@ -1471,6 +1471,7 @@ int tffft_consistency(tffft_plan_t pl, double* residue) {
   CUDA_TRY(cudaSetDevice(pl->comm->device));
   if (!pl->s1_fused) {  // fold the c2r row records into per-plane maxima
     reduce_row_stats_kernel<<<pl->n0p, 256, 0, pl->last_inverse_stream>>>(pl->row_stats, pl->n1, pl->stats);
+    pl->launches++;
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaStreamSynchronize(pl->last_inverse_stream));

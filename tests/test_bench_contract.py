@@ -43,6 +43,6 @@ def test_gpu_arm_line():
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.5 and r["unit"] == "GB/s"
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] == 128 ** 3 * 8 and e["d2h_bytes_per_step"] == 128 ** 3 * 8
-    assert d["gpu_launches"] == 6 * 3  # six kernels per forward + inverse pair
+    assert d["gpu_launches"] == 7 * 3  # six FFT kernels + the consistency reduction per pair
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["cpu_baseline"]["value"] > 0
