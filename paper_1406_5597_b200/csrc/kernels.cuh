@@ -183,8 +183,10 @@ __host__ __device__ constexpr int r2c_radix_bits(int L, int real_bytes) {
 #ifndef TFFFT_C2R_L9_F64_MB
 #define TFFFT_C2R_L9_F64_MB 4
 #endif
+// (and for n2 = 512: radix 8 at 5 CTAs/SM, 0.392 -> 0.379 ms per 512^3 launch;
+// the r2c rows there keep radix 16, profiles/r01s13/rows_512.txt)
 __host__ __device__ constexpr int c2r_radix_bits(int L, int real_bytes) {
-  return (L == 9 && real_bytes == 8) ? TFFFT_C2R_L9_F64_MB : 0;
+  return real_bytes == 8 ? (L == 9 ? TFFFT_C2R_L9_F64_MB : (L == 8 ? 3 : 0)) : 0;
 }
 
 template <int L, int MB = 0> struct RowCfg {
@@ -200,7 +202,7 @@ template <int L, int MB = 0> struct RowCfg {
   // 2.69 ms per 1024^3 launch), c2r -- with its consistency statistics and
   // pair loads -- at 5 (94 registers, 2.88 ms).  Other lengths keep the default.
   // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
-  static constexpr bool CAP = L == 9 && THREADS == 128 && Shape<L, MB>::E == 8;
+  static constexpr bool CAP = (L == 9 || L == 8) && THREADS == 128 && Shape<L, MB>::E == 8;
   static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
   static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
 };
