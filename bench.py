@@ -203,7 +203,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{n0}x{n1}x{n2} float64 r2c+c2r pair", "grid": [n0, n1, n2], "p": 1},
+        # the GPU arm's config (same workload string, grid and slab count); the
+        # CPU port computes the whole pair, which is what p slabs compute together
+        "config": {"workload": f"{n0}x{n1}x{n2} float64 r2c+c2r pair, slab p={args.gpus}",
+                   "grid": [n0, n1, n2], "p": args.gpus, "parallelism": f"slab{args.gpus}"},
         "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

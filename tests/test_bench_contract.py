@@ -30,6 +30,9 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["unit"] == "GFLOP/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the GPU arm's workload string, so the driver's ratio compares like with like
+    assert d["config"]["workload"] == "32x32x32 float64 r2c+c2r pair, slab p=1"
+    assert d["config"]["parallelism"] == "slab1"
 
 
 @pytest.mark.gpu
