@@ -103,7 +103,17 @@ class ClockSampler:
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-        watts = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+        # instantaneous board power: nvmlDeviceGetPowerUsage is a 1 s average,
+        # which lags a sub-second timed region that starts from idle
+        watts = None
+        try:
+            fv = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_POWER_INSTANT])[0]
+            if fv.nvmlReturn == 0:
+                watts = fv.value.uiVal / 1000.0
+        except Exception:
+            pass
+        if watts is None:
+            watts = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
         return (float(sm), float(mx), {n for n, b in self._bits.items() if bits & b}, watts)
 
     def _sample_smi(self):

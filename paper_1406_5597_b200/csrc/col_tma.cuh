@@ -32,6 +32,13 @@
 
 namespace tffft {
 
+// column-kernel store flavour: 0 plain, 1 L2 cache-hint policy, 2 st.global.cs
+#ifndef TFFFT_COL_STORE
+#define TFFFT_COL_STORE 0
+#endif
+__device__ __forceinline__ void st_cs(cx<double>* a, cx<double> z) { __stcs(reinterpret_cast<double2*>(a), make_double2(z.x, z.y)); }
+__device__ __forceinline__ void st_cs(cx<float>* a, cx<float> z) { __stcs(reinterpret_cast<float2*>(a), make_float2(z.x, z.y)); }
+
 template <typename T, int L, bool WIDE>
 struct TmaColCfg {
   using CF = ColCfg<T, L, WIDE>;
@@ -175,7 +182,16 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
 #pragma unroll
       for (int u = 0; u < E / SH::RL; ++u)
 #pragma unroll
-        for (int m = 0; m < SH::RL; ++m) col[(unsigned)SH::out_elem(tt, u, m) * rs] = v[u * SH::RL + m];
+        for (int m = 0; m < SH::RL; ++m) {
+          cx<T>* a = col + (unsigned)SH::out_elem(tt, u, m) * rs;
+#if TFFFT_COL_STORE == 1
+          st_hint(a, v[u * SH::RL + m], pol);  // the loads' L2 policy on the stores too
+#elif TFFFT_COL_STORE == 2
+          st_cs(a, v[u * SH::RL + m]);  // streaming (evict-first) stores
+#else
+          *a = v[u * SH::RL + m];
+#endif
+        }
     }
     cur = nxt;
   }
