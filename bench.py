@@ -160,11 +160,15 @@ class ClockSampler:
 # CPU oracle (reference path port): bounded sample of the same workload
 # ---------------------------------------------------------------------------
 
-def cpu_sample(n0, n1, n2, planes=8, workers=None):
+def cpu_sample(n0, n1, n2, planes=64, workers=None):
     """Time the oracle (restatement of the reference's STRIDED pipeline,
-    bit-identical to it) on a bounded sample of the full-size workload and
-    extrapolate: stage 1 + 1' on `planes` of the n0 planes, stage 3 + 3' on
-    the same fraction of the n1*n2c columns (gather -> c2c -> scatter)."""
+    bit-identical to it) on a bounded sample of the full-size p = 1 pair:
+    stage 1 + 1' (r2c rows, n1 columns and back) on `planes` of the n0
+    planes, and stage 3 + 3' on the same fraction of the n1*n2c STRIDED_INPLACE
+    columns, gathered and scattered at their true two-level offsets
+    (layout.py:189-219) in a full-size spectral buffer.  Returns the MEASURED
+    throughput of the sample (its own flops / its own seconds), the measured
+    seconds, the threads used and a description.  Nothing is extrapolated."""
     import numpy as np
 
     import oracle
@@ -174,27 +178,56 @@ def cpu_sample(n0, n1, n2, planes=8, workers=None):
     rng = np.random.default_rng(0)
     slab = rng.uniform(-1.0, 1.0, size=(planes, n1, n2))
     ncols = max(1, (n1 * n2c * planes) // n0)
+    # full-size STRIDED_INPLACE buffer (p = 1: element r of column c at r*n1*n2c + c);
+    # np.zeros maps pages lazily, so only the sampled columns' rows are touched
+    flat = np.zeros(n0 * n1 * n2c, dtype=np.complex128)
+    row = np.arange(n0, dtype=np.int64) * (n1 * n2c)
+    blk = max(1, -(-ncols // (4 * workers)))
+    spans = [(a, min(a + blk, ncols)) for a in range(0, ncols, blk)]
+    for a, b in spans:
+        offs = np.arange(a, b, dtype=np.int64)[:, None] + row[None, :]
+        flat[offs] = rng.standard_normal(offs.shape) + 1j * rng.standard_normal(offs.shape)
     t0 = time.perf_counter()
     spec = oracle.stage1_forward(slab, workers)
     oracle.stage1_inverse(spec, n2, workers)
     t1 = time.perf_counter()
-    # stage 3 on ncols columns of length n0 laid out (n0, ncols): same gather/scatter pattern
-    flat = (rng.standard_normal((n0, ncols)) + 1j * rng.standard_normal((n0, ncols))).reshape(-1)
-    offs = (np.arange(n0)[None, :] * ncols + np.arange(ncols)[:, None])
     for inv in (False, True):
         def work(a, b, inv=inv):
-            cols = flat[offs[a:b]]
+            offs = np.arange(a, b, dtype=np.int64)[:, None] + row[None, :]
+            cols = flat[offs]
             oracle.c2c_rows(cols, inv)
-            flat[offs[a:b]] = cols
-        oracle.slabfft_oracle._run(work, oracle.slabfft_oracle._chunks(ncols, workers), workers)
+            flat[offs] = cols
+        oracle.slabfft_oracle._run(work, spans, workers)
     t2 = time.perf_counter()
-    scale1 = n0 / planes
-    scale3 = (n1 * n2c) / ncols
-    t_full = (t1 - t0) * scale1 + (t2 - t1) * scale3
-    sample = (f"oracle port, {workers} threads: stage 1+1' on {planes}/{n0} planes and stage 3+3' on "
-              f"{ncols}/{n1 * n2c} columns of the {n0}x{n1}x{n2} float64 pair, extrapolated "
-              f"({t2 - t0:.1f} s measured)")
-    return pair_flops(n0, n1, n2) / t_full / 1e9, t_full, workers, sample
+    # flops of the sample: the pair's 2 * 2.5 N log2 N split over the axes as the
+    # passes that ran (stage 1+1': planes/n0 of the n1 and n2 axis work; stage
+    # 3+3': ncols/(n1*n2c) of the n0 axis work)
+    n = n0 * n1 * n2
+    f_axis = lambda L: 2 * 2.5 * n * math.log2(L)
+    flops = f_axis(n1 * n2) * planes / n0 + f_axis(n0) * ncols / (n1 * n2c)
+    secs = t2 - t0
+    sample = (f"oracle port (bit-identical to the reference), {workers} threads, measured on a sample of the "
+              f"{n0}x{n1}x{n2} float64 p=1 pair: stage 1+1' on {planes}/{n0} planes ({t1 - t0:.2f} s) and "
+              f"stage 3+3' on {ncols}/{n1 * n2c} columns at their STRIDED_INPLACE offsets ({t2 - t1:.2f} s); "
+              f"value = the sample's flops / its measured seconds")
+    return flops / secs / 1e9, secs, workers, sample
+
+
+def full_pair_record():
+    """The one full-size CPU pair measured on the GPU host (tools/cpu_full_pair.py), if committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_full_pair.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cube_config(n0, n1, n2, dt, p):
+    """The config object both arms print (identical keys and values)."""
+    s_r = 8 if dt == "float64" else 4
+    return {"workload": f"{n0}x{n1}x{n2} {dt} r2c+c2r pair, slab p={p}",
+            "grid": [n0, n1, n2], "p": p, "parallelism": f"slab{p}",
+            "l2": f"inputs larger than L2 ({n0 // p * n1 * n2 * s_r / 1e9:.2f} GB real slab per GPU)"}
 
 
 def run_reference(args):
@@ -202,24 +235,29 @@ def run_reference(args):
     if rank != 0:
         return 0
     n0 = n1 = n2 = args.grid
+    # one step = one measured sample of the workload (cpu_sample); ms_per_step is
+    # that measured time, so steps x ms_per_step is the real timed region
     vals = []
     for i in range(args.warmup + args.steps):
-        gf, t_full, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
+        gf, secs, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
         if i >= args.warmup:
-            vals.append((gf, t_full))
+            vals.append((gf, secs))
     gf = statistics.median(v[0] for v in vals)
     ms = statistics.median(v[1] for v in vals) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        # the GPU arm's config (same workload string, grid and slab count); the
-        # CPU port computes the whole pair, which is what p slabs compute together
-        "config": {"workload": f"{n0}x{n1}x{n2} float64 r2c+c2r pair, slab p={args.gpus}",
-                   "grid": [n0, n1, n2], "p": args.gpus, "parallelism": f"slab{args.gpus}"},
-        "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        # the GPU arm's config object, key for key; the CPU port computes the whole
+        # pair, which is what the p slabs compute together
+        "config": cube_config(n0, n1, n2, "float64", args.gpus),
+        "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample,
+                         "timed_steps_s": [round(v[1], 3) for v in vals]},
         "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    full = full_pair_record()
+    if full and full.get("grid") == [n0, n1, n2]:
+        line["cpu_full_pair"] = full
     print(json.dumps(line))
     return 0
 
@@ -238,8 +276,7 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -376,12 +413,11 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64" if dt == "float64" else "f32",
         "data": "synthetic: seeded uniform[-1,1) real field generated on device",
-        "config": {
-            "workload": (f"{n0}x{n1}x{n2} {dt} r2c+c2r pair, slab p={p}" if ncomp == 1 else
-                         f"turbulence: 3 x {n0}x{n1}x{n2} {dt} components, batched inverse c2r then forward r2c, "
-                         f"slab p={p}"),
-            "grid": [n0, n1, n2], "p": p, "parallelism": f"slab{p}",
-            "l2": f"inputs larger than L2 ({n0p * n1 * n2 * s_r / 1e9:.2f} GB real slab per GPU)",
+        "config": (cube_config(n0, n1, n2, dt, p) if ncomp == 1 else
+                   dict(cube_config(n0, n1, n2, dt, p),
+                        workload=(f"turbulence: 3 x {n0}x{n1}x{n2} {dt} components, batched inverse c2r then "
+                                  f"forward r2c, slab p={p}"))),
+        "details": {
             "pair_roofline_ms": t_roof, "pair_roofline_frac": t_roof / ms,
             "stage_ms_per_pair": {"stage1+1'": st1_ms * 2,
                                   "exchange": stages["exchange_us"] / 1e3 / (args.steps * ncomp),
@@ -404,6 +440,9 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "cube":
         gf, _, cores, sample = cpu_sample(n0, n1, n2, planes=args.cpu_planes)
         line["cpu_baseline"] = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample}
+        full = full_pair_record()
+        if full and full.get("grid") == [n0, n1, n2] and dt == "float64":
+            line["cpu_full_pair"] = full
     if rank == 0:
         print(json.dumps(line))
     fp.close()
@@ -423,12 +462,28 @@ def main():
     ap.add_argument("--config", choices=["cube", "turbulence"], default="cube",
                     help="cube: seeded uniform field pair (headline); turbulence: BASELINE config 5")
     ap.add_argument("--e2e-steps", type=int, default=8)
-    ap.add_argument("--cpu-planes", type=int, default=128)
+    ap.add_argument("--cpu-planes", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
     return run_gpu(args)
+
+
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: re-run this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1;
+    rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -137,9 +137,14 @@ def c2r_rows(half: np.ndarray, n: int) -> tuple[np.ndarray, float]:
 # stage 1 / 1' : per-plane 2D transforms (kernels.py:262-303, dfft.py:161-163, 205-209)
 # ---------------------------------------------------------------------------
 
-def _chunks(count: int, workers: int):
+def _chunks(count: int, workers: int, max_step: int | None = None):
+    """Spans of [0, count) for `workers` threads; `max_step` bounds a span so
+    the per-span temporaries stay small at full size (1024^3).  Batching rows
+    differently does not change a bit of the result (kernels.py:134-140)."""
     workers = max(1, min(workers, count))
     step = -(-count // workers)
+    if max_step:
+        step = max(1, min(step, max_step))
     return [(a, min(a + step, count)) for a in range(0, count, step)]
 
 
@@ -163,7 +168,7 @@ def stage1_forward(slab: np.ndarray, workers: int = 1) -> np.ndarray:
         c2c_rows(cols, inverse=False)
         out[a:b] = cols.reshape(b - a, n2c, n1).transpose(0, 2, 1)
 
-    _run(work, _chunks(n0p, workers), workers)
+    _run(work, _chunks(n0p, workers, max(1, (1 << 22) // (n1 * n2))), workers)
     return out
 
 
@@ -184,7 +189,7 @@ def stage1_inverse(buf: np.ndarray, n2: int, workers: int = 1) -> tuple[np.ndarr
             res = max(res, r)
         return res
 
-    res = _run(work, _chunks(n0p, workers), workers)
+    res = _run(work, _chunks(n0p, workers, max(1, (1 << 22) // (n1 * n2))), workers)
     return out, max(res) if res else 0.0
 
 
@@ -227,14 +232,19 @@ def stage3(flat: np.ndarray, n0: int, n1: int, n2: int, p: int, inverse: bool,
            workers: int = 1) -> None:
     """Length-n0 c2c over every owned column, gathered by its two-level
     stride, transformed and scattered back (kernels.py:176-200, dfft.py:170-171, 196-197)."""
-    offs = strided_column_offsets(n0, n1, n2, p)
+    n0p, n1p, n2c = n0 // p, n1 // p, n2 // 2 + 1
+    r = np.arange(n0, dtype=np.int64)
+    col = (r % n0p) * (n1 * n2c) + (r // n0p) * (n1p * n2c)  # TwoLevelStride of column 0
 
     def work(a, b):
-        cols = flat[offs[a:b]]
+        # rows a..b of strided_column_offsets, built per span (the full table is
+        # ncols x n0 int64: 4.3 GB at 1024^3)
+        offs = np.arange(a, b, dtype=np.int64)[:, None] + col[None, :]
+        cols = flat[offs]
         c2c_rows(cols, inverse)
-        flat[offs[a:b]] = cols
+        flat[offs] = cols
 
-    _run(work, _chunks(offs.shape[0], workers), workers)
+    _run(work, _chunks(n1p * n2c, workers, max(1, (1 << 22) // n0)), workers)
 
 
 def forward_all(field: np.ndarray, p: int, workers: int = 1) -> list[np.ndarray]:

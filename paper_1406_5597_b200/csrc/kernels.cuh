@@ -311,16 +311,17 @@ col_fft_kernel(const ColParams prm) {
   // (the host passes a counter only where it was measured faster: columns of 1024+)
   constexpr bool DYN_OK = TFFFT_COL_TICKET && CF::XCHG && CL == 1;
   const bool dyn = DYN_OK && prm.ticket != nullptr;
-  __shared__ long long s_tk[2];
+  // s_tk[0..1]: ping-pong next-tile slots; s_tk[2]: the first tile, in its own
+  // slot so thread 0's first ping-pong write cannot race a late warp's read
+  __shared__ long long s_tk[3];
   long long it = 0;
   if (dyn) {
     if (t == 0) {
-      tile = (long long)atomicAdd(prm.ticket, 1ull);
+      s_tk[2] = (long long)atomicAdd(prm.ticket, 1ull);
       s_tk[0] = (long long)atomicAdd(prm.ticket, 1ull);
-      s_tk[1] = tile;  // published with the barrier below
     }
     __syncthreads();
-    tile = s_tk[1];
+    tile = s_tk[2];
   }
   if (tile >= ntiles) return;
   Col cur = column(tile);

@@ -1,6 +1,7 @@
 // Explicit instantiation + runtime dispatch of the stage kernels for one
 // precision.  Included by kernels_f64.cu / kernels_f32.cu with TFFFT_REAL set.
 #include <algorithm>
+#include <atomic>
 
 #include "kernels.cuh"
 #include "fourstep.cuh"
@@ -10,20 +11,55 @@
 
 namespace tffft {
 
+// Per-device launch state.  cudaFuncSetAttribute(MaxDynamicSharedMemorySize)
+// and the occupancy / SM-count queries apply to the current device only, so a
+// process that plans on several devices (comm_init_all, make_communicators on
+// device 1 after device 0) caches them per device.
+constexpr int kMaxDevices = 64;
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : d % kMaxDevices;
+}
+
+// one per kernel instantiation (a static of its launcher)
+struct KernelCache {
+  std::atomic<unsigned long long> prepped{0};  // bit d: smem attribute set on device d
+  std::atomic<int> occ[kMaxDevices] = {};      // resident CTAs per SM on device d (0: not queried)
+};
+
 template <typename K>
-static cudaError_t prep_smem(K kernel, size_t bytes) {
+static cudaError_t prep_smem(K kernel, KernelCache& kc, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const unsigned long long bit = 1ull << current_device();
+  if (kc.prepped.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) kc.prepped.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// resident CTAs per SM of `kernel` on the current device (after prep_smem)
+template <typename K>
+static int occupancy(K kernel, KernelCache& kc, int threads, size_t smem) {
+  std::atomic<int>& c = kc.occ[current_device()];
+  int n = c.load(std::memory_order_relaxed);
+  if (n > 0) return n;
+  n = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  n = n < 1 ? 1 : n;
+  c.store(n, std::memory_order_relaxed);
+  return n;
 }
 
 static int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
+  static std::atomic<int> cache[kMaxDevices] = {};
+  const int dev = current_device();
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev].store(v, std::memory_order_relaxed);
+  return v;
 }
 
 template <typename T, int L, bool INV, bool TWO, int RD, bool WIDE>
@@ -31,13 +67,10 @@ static cudaError_t col_one(const ColParams& p, cudaStream_t s) {
   using CF = ColCfg<T, L, WIDE>;
   const size_t sm = col_smem_bytes<T, L, WIDE>();
   auto k = col_fft_kernel<T, L, INV, TWO, RD, WIDE>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
-  static int per_sm = [&] {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, CF::THREADS, sm);
-    return n < 1 ? 1 : n;
-  }();
+  const int per_sm = occupancy(k, kc, CF::THREADS, sm);
   const long long tiles = (p.ncols + CF::CL * CF::B - 1) / (CF::CL * CF::B);
   if (tiles <= 0) return cudaSuccess;
   long long blocks = CF::PERSISTENT ? std::min<long long>(tiles * CF::CL, (long long)per_sm * num_sms())
@@ -69,7 +102,8 @@ static cudaError_t r2c_one(const RowParams& p, cudaStream_t s) {
   using RC = RowCfg<L, r2c_radix_bits(L, sizeof(T))>;
   const size_t sm = row_smem_bytes<T, L, r2c_radix_bits(L, sizeof(T))>();
   auto k = r2c_rows_kernel<T, L>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
   const long long blocks = (p.nrows + RC::B - 1) / RC::B;
   if (blocks <= 0) return cudaSuccess;
@@ -83,7 +117,8 @@ static cudaError_t c2r_one(const RowParams& p, cudaStream_t s) {
   using RC = RowCfg<L, c2r_radix_bits(L, sizeof(T))>;
   const size_t sm = row_smem_bytes<T, L, c2r_radix_bits(L, sizeof(T))>();
   auto k = c2r_rows_kernel<T, L>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
   const long long blocks = (p.nrows + RC::B - 1) / RC::B;
   if (blocks <= 0) return cudaSuccess;
@@ -156,13 +191,10 @@ template <typename T, int LA, int LB, bool INV, bool TWO, bool REDIR>
 static cudaError_t fs_one(const FourStepParams& p, cudaStream_t s) {
   const size_t sm = fourstep_smem_bytes<T, LA, LB>();
   auto k = fourstep_kernel<T, LA, LB, INV, TWO, REDIR>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
-  static int per_sm = [&] {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFsThreads, sm);
-    return n < 1 ? 1 : n;
-  }();
+  const int per_sm = occupancy(k, kc, kFsThreads, sm);
   (void)cudaGetLastError();
   k<<<(unsigned)(per_sm * num_sms()), kFsThreads, sm, s>>>(p);
   return cudaGetLastError();
@@ -184,13 +216,10 @@ template <typename T, int LR, int LC, bool FWD, bool REDIR>
 static cudaError_t s1_one(const Stage1Params& p, cudaStream_t s) {
   const size_t sm = S1Cfg<T, LR, LC>::SMEM;
   auto k = stage1_fused_kernel<T, LR, LC, FWD, REDIR>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
-  static int per_sm = [&] {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kS1Threads, sm);
-    return n < 1 ? 1 : n;
-  }();
+  const int per_sm = occupancy(k, kc, kS1Threads, sm);
   (void)cudaGetLastError();
   k<<<(unsigned)(per_sm * num_sms()), kS1Threads, sm, s>>>(p);
   return cudaGetLastError();
@@ -219,13 +248,10 @@ template <typename T, int LA, int LB, bool INV>
 static cudaError_t ft_one(const CUtensorMap* maps, const FsTmaParams& p, cudaStream_t s) {
   const size_t sm = FtCfg<T, LA, LB>::SMEM;
   auto k = fourstep_tma_kernel<T, LA, LB, INV>;
-  static cudaError_t prep = prep_smem(k, sm);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, sm);
   if (prep != cudaSuccess) return prep;
-  static int per_sm = [&] {
-    int n = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kFtThreads, sm);
-    return n < 1 ? 1 : n;
-  }();
+  const int per_sm = occupancy(k, kc, kFtThreads, sm);
   (void)cudaGetLastError();
   k<<<(unsigned)(per_sm * num_sms()), kFtThreads, sm, s>>>(maps[0], maps[1], maps[2], maps[3], p);
   return cudaGetLastError();
@@ -248,7 +274,8 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
     return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
   } else {
   auto k = col_tma_kernel<T, L, INV, WIDE>;
-  static cudaError_t prep = prep_smem(k, TC::SMEM);
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, TC::SMEM);
   if (prep != cudaSuccess) return prep;
   if (p.ntiles <= 0) return cudaSuccess;
   const long long blocks = std::min<long long>(p.ntiles, num_sms());

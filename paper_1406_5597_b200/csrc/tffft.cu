@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -137,7 +138,9 @@ struct LocalFabric {
     std::vector<void*> staging, landing;
     std::vector<cudaEvent_t> ready, done;
   };
-  std::vector<Slot> slots;
+  // a deque: slot(seq) may grow it while other ranks hold references to
+  // earlier slots (growing a deque at the end keeps references valid)
+  std::deque<Slot> slots;
   std::atomic<int> refs{0};
 
   explicit LocalFabric(int p_, int dev) : p(p_), device(dev) {}
@@ -194,9 +197,13 @@ struct tffft_comm_s {
 // plans
 // ---------------------------------------------------------------------------
 struct StageEvents {
-  cudaEvent_t e[4];
-  bool forward;
+  cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool forward = true;
+  bool pending = false;  // recorded, not yet folded into the plan's stage totals
 };
+// events are created once (set_timing) and reused round robin, so no event is
+// created inside a timed region
+constexpr int kEventRing = 128;
 
 struct tffft_plan_s {
   tffft_comm_t comm = nullptr;
@@ -237,7 +244,9 @@ struct tffft_plan_s {
   int tma_cols = 0;      // TMA-fed column passes: 0 off, 1 every supported pass, 2 the measured winners
   size_t workspace = 0;
   bool timing = false;
-  std::vector<StageEvents> events;
+  std::vector<StageEvents> events;  // kEventRing slots while timing is enabled
+  int event_next = 0;
+  double stage_ms[3] = {0.0, 0.0, 0.0};
   uint64_t counters[3] = {0, 0, 0};
   uint64_t launches = 0;
   cudaStream_t last_inverse_stream = nullptr;
@@ -1274,8 +1283,26 @@ int tffft_plan_sizes(tffft_plan_t pl, int64_t* re, int64_t* sp) {
 
 static void free_events(tffft_plan_t pl) {
   for (auto& ev : pl->events)
-    for (auto& e : ev.e) cudaEventDestroy(e);
+    for (auto& e : ev.e)
+      if (e) cudaEventDestroy(e);
   pl->events.clear();
+  pl->event_next = 0;
+}
+
+// fold one recorded call into the stage totals
+// (forward: stage1, exchange, stage3; inverse: stage3', exchange, stage1')
+static int harvest(tffft_plan_t pl, StageEvents& ev) {
+  if (!ev.pending) return TFFFT_OK;
+  CUDA_TRY(cudaEventSynchronize(ev.e[3]));
+  float a, b, c;
+  CUDA_TRY(cudaEventElapsedTime(&a, ev.e[0], ev.e[1]));
+  CUDA_TRY(cudaEventElapsedTime(&b, ev.e[1], ev.e[2]));
+  CUDA_TRY(cudaEventElapsedTime(&c, ev.e[2], ev.e[3]));
+  pl->stage_ms[ev.forward ? 0 : 2] += a;
+  pl->stage_ms[1] += b;
+  pl->stage_ms[ev.forward ? 2 : 0] += c;
+  ev.pending = false;
+  return TFFFT_OK;
 }
 
 int tffft_plan_destroy(tffft_plan_t pl) {
@@ -1306,12 +1333,18 @@ static int check_ptr(const void* ptr, const char* what, size_t align) {
 static int begin_events(tffft_plan_t pl, bool fwd, cudaStream_t s, StageEvents** ev) {
   *ev = nullptr;
   if (!pl->timing) return TFFFT_OK;
-  StageEvents e{};
+  if (pl->events.empty()) {  // timing enabled without set_timing (defensive)
+    pl->events.resize(kEventRing);
+    for (auto& x : pl->events)
+      for (auto& e : x.e) CUDA_TRY(cudaEventCreate(&e));
+  }
+  StageEvents& e = pl->events[pl->event_next];
+  pl->event_next = (pl->event_next + 1) % kEventRing;
+  TRY(harvest(pl, e));  // a slot still pending from kEventRing calls ago
   e.forward = fwd;
-  for (auto& x : e.e) CUDA_TRY(cudaEventCreate(&x));
-  pl->events.push_back(e);
-  *ev = &pl->events.back();
-  CUDA_TRY(cudaEventRecord((*ev)->e[0], s));
+  e.pending = true;
+  *ev = &e;
+  CUDA_TRY(cudaEventRecord(e.e[0], s));
   return TFFFT_OK;
 }
 
@@ -1424,23 +1457,19 @@ int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
 int tffft_set_timing(tffft_plan_t pl, int enable) {
   if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
   pl->timing = enable != 0;
+  if (pl->timing && pl->events.empty()) {
+    CUDA_TRY(cudaSetDevice(pl->comm->device));
+    pl->events.resize(kEventRing);
+    for (auto& x : pl->events)
+      for (auto& e : x.e) CUDA_TRY(cudaEventCreate(&e));
+  }
   return TFFFT_OK;
 }
 
 int tffft_stage_times(tffft_plan_t pl, double ms[3]) {
   if (!pl || !ms) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
-  ms[0] = ms[1] = ms[2] = 0.0;
-  for (auto& ev : pl->events) {
-    CUDA_TRY(cudaEventSynchronize(ev.e[3]));
-    float a, b, c;
-    CUDA_TRY(cudaEventElapsedTime(&a, ev.e[0], ev.e[1]));
-    CUDA_TRY(cudaEventElapsedTime(&b, ev.e[1], ev.e[2]));
-    CUDA_TRY(cudaEventElapsedTime(&c, ev.e[2], ev.e[3]));
-    // forward: stage1, exchange, stage3; inverse: stage3', exchange, stage1'
-    ms[ev.forward ? 0 : 2] += a;
-    ms[1] += b;
-    ms[ev.forward ? 2 : 0] += c;
-  }
+  for (auto& ev : pl->events) TRY(harvest(pl, ev));
+  for (int i = 0; i < 3; ++i) ms[i] = pl->stage_ms[i];
   return TFFFT_OK;
 }
 
@@ -1452,7 +1481,8 @@ int tffft_counters(tffft_plan_t pl, uint64_t b[3]) {
 
 int tffft_reset_instrumentation(tffft_plan_t pl) {
   if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
-  free_events(pl);
+  for (auto& ev : pl->events) ev.pending = false;
+  pl->stage_ms[0] = pl->stage_ms[1] = pl->stage_ms[2] = 0.0;
   pl->counters[0] = pl->counters[1] = pl->counters[2] = 0;
   pl->launches = 0;
   return TFFFT_OK;

@@ -33,6 +33,32 @@ def test_reference_arm_line():
     # the GPU arm's workload string, so the driver's ratio compares like with like
     assert d["config"]["workload"] == "32x32x32 float64 r2c+c2r pair, slab p=1"
     assert d["config"]["parallelism"] == "slab1"
+    # measured, not extrapolated: the timed steps are the reported step time
+    assert len(d["cpu_baseline"]["timed_steps_s"]) == 1
+    assert abs(d["cpu_baseline"]["timed_steps_s"][0] * 1e3 - d["ms_per_step"]) < 1.0 + 1e-3 * d["ms_per_step"]
+
+
+def test_reference_arm_config_matches_gpu_arm():
+    """Both arms print the same config object (bench.cube_config), key for key."""
+    import bench
+
+    d = _run(["--impl", "reference", "--grid", "32", "--steps", "1", "--warmup", "0", "--cpu-planes", "8"])
+    assert d["config"] == bench.cube_config(32, 32, 32, "float64", 1)
+
+
+def test_gpus_n_without_torchrun_self_launches(monkeypatch):
+    """--gpus N > 1 outside torchrun re-executes itself under torch.distributed.run."""
+    import bench
+
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    assert bench.main() == 0
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
 
 
 @pytest.mark.gpu
@@ -41,7 +67,7 @@ def test_gpu_arm_line():
     stage-3 kernel, host-buffer e2e, launch count, clocks, cpu_baseline."""
     d = _run(["--grid", "128", "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--cpu-planes", "8"])
     assert BASE_KEYS <= set(d)
-    assert d["n_gpus"] == 1 and d["value"] > 0 and d["config"]["roundtrip_rel_l2"] <= 1e-12
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["details"]["roundtrip_rel_l2"] <= 1e-12
     r = d["roofline"]
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.5 and r["unit"] == "GB/s"
     e = d["e2e"]
