@@ -13,6 +13,9 @@
  *   tffft_inverse          <- slabfft.dfft.inverse         pkg/src/slabfft/dfft.py:179-215
  *   tffft_comm_init_local  <- slabfft.transport.make_communicators  transport.py:425-430
  *   tffft_comm_init_rank   <- (MPI communicator; NCCL over NVLink)
+ *   tffft_comm_init_all    <- slabfft.transport.run_spmd across GPUs   transport.py:425-468
+ *   tffft_comm_init_ipc    <- Endpoint.all_to_all over process-shared memory  transport.py:359-419
+ *   tffft_plan_create_batched <- dfft.plan + a batch of fields  dfft.py:93-145
  *   tffft_stage_times      <- FftPlan.timers_us            dfft.py:84-90, 173-175
  *   tffft_counters         <- CopyCounter.snapshot         transport.py:97-114
  *   tffft_consistency      <- FftPlan.last_imag_residue + ConsistencyError  dfft.py:73,211; kernels.py:212-239
@@ -50,6 +53,9 @@ enum { TFFFT_PAIRWISE = 0, TFFFT_COLLECTIVE = 1 };
 
 typedef struct tffft_comm_s* tffft_comm_t;
 typedef struct tffft_plan_s* tffft_plan_t;
+/* host barrier of an IPC communicator: returns 0 once every rank has entered
+ * it, non-zero on failure (the plan's call then fails with TFFFT_ERR_TRANSPORT) */
+typedef int (*tffft_barrier_fn)(void* ctx);
 
 const char* tffft_last_error(void);
 int tffft_version(void);
@@ -63,6 +69,18 @@ int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tff
  * in-process multi-rank fabric, transport.py:188-302).  Each endpoint is
  * driven by its own host thread; forward/inverse are collectives. */
 int tffft_comm_init_local(int p, int device, tffft_comm_t* comms);
+/* Single process driving p GPUs (ncclCommInitAll over devices[0..p-1], one
+ * device per rank): the reference's run_spmd (transport.py:425-468) across
+ * GPUs, one host thread per communicator. */
+int tffft_comm_init_all(int p, const int* devices, tffft_comm_t* comms);
+/* One process per rank, exchange over CUDA IPC: each plan exports its exchange
+ * buffers and events (tffft_plan_ipc_export), the caller all-gathers the blobs
+ * and every rank attaches the peers' (tffft_plan_ipc_attach).  The exchange is
+ * a device pull from the peers' staging (or, with TFFFT_FLAG_PEER_STORES, the
+ * producing stage's stores into the peers' landing buffers), ordered by IPC
+ * events; `barrier` is the only host-side collective (MPI, a gloo group, ...).
+ * Ranks may share a device (several processes on one GPU) or not (P2P). */
+int tffft_comm_init_ipc(int p, int rank, int device, tffft_barrier_fn barrier, void* ctx, tffft_comm_t* comm);
 /* asynchronous communicator failure (ncclCommGetAsyncError) as TFFFT_ERR_TRANSPORT;
  * TFFFT_OK for a healthy or local communicator (transport.py:209-219 abort propagation) */
 int tffft_comm_check(tffft_comm_t comm);
@@ -98,6 +116,24 @@ enum {
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* plan);
+/* Batched plan (SURVEY.md §8(b) plan_create(..., batch, ...)): every forward /
+ * inverse call transforms `batch` fields stored back to back (real slabs of
+ * n0/p*n1*n2, spectral slabs of n0/p*n1*(n2/2+1) elements).  p = 1: each stage
+ * is ONE launch over all fields; p > 1: a two-deep pipeline in which field c's
+ * exchange (on the plan's exchange stream) overlaps field c+1's producing
+ * stage.  The inverse's consistency statistics cover every field and are
+ * checked once per call (tffft_consistency).  The optional fused-stage-1 and
+ * four-step schedules are single-field (dropped when batch > 1). */
+int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, int flags, int batch,
+                              tffft_comm_t comm, tffft_plan_t* plan);
+int tffft_plan_batch(tffft_plan_t plan, int* batch);
+/* CUDA IPC exchange buffers of NCCL (peer stores) and IPC plans, p > 1.  The
+ * blob holds, per buffer set, handles of the staging and landing buffers and
+ * (IPC communicators) of the ready / done events.  attach takes p blobs in rank
+ * order and is collective. */
+int tffft_plan_ipc_blob_bytes(tffft_plan_t plan, size_t* bytes);
+int tffft_plan_ipc_export(tffft_plan_t plan, uint8_t* blob);
+int tffft_plan_ipc_attach(tffft_plan_t plan, const uint8_t* blobs);
 /* Fused exchange on an NCCL communicator (TFFFT_FLAG_PEER_STORES, p > 1): each
  * rank exports a CUDA IPC handle of its landing buffer, the handles are
  * all-gathered by the caller (rank order, 64 bytes each), and attach_peers

@@ -22,6 +22,9 @@ _SIGS = {
     "tffft_get_unique_id": (_c.c_int, [_c.c_char_p]),
     "tffft_comm_init_rank": (_c.c_int, [_c.c_int, _c.c_int, _c.c_char_p, _c.c_int, _c.POINTER(_c.c_void_p)]),
     "tffft_comm_init_local": (_c.c_int, [_c.c_int, _c.c_int, _c.POINTER(_c.c_void_p)]),
+    "tffft_comm_init_all": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_void_p)]),
+    "tffft_comm_init_ipc": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p,
+                                       _c.POINTER(_c.c_void_p)]),
     "tffft_comm_check": (_c.c_int, [_c.c_void_p]),
     "tffft_comm_rank": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_comm_size": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
@@ -32,6 +35,12 @@ _SIGS = {
                                      _c.POINTER(_c.c_void_p)]),
     "tffft_plan_create_ex": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
                                         _c.c_void_p, _c.POINTER(_c.c_void_p)]),
+    "tffft_plan_create_batched": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
+                                             _c.c_int, _c.c_void_p, _c.POINTER(_c.c_void_p)]),
+    "tffft_plan_batch": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
+    "tffft_plan_ipc_blob_bytes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_size_t)]),
+    "tffft_plan_ipc_export": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
+    "tffft_plan_ipc_attach": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "tffft_plan_flags": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_plan_landing_handle": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "tffft_plan_attach_peers": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
@@ -51,6 +60,9 @@ _SIGS = {
     "tffft_radix_schedule": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
 }
 SYMBOLS = tuple(_SIGS)
+
+# C type of tffft_barrier_fn (include/tffft.h): int (*)(void* ctx)
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
 
 _lock = threading.Lock()
 _lib = None

@@ -75,6 +75,7 @@ struct NcclApi {
   std::string err;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
@@ -109,6 +110,7 @@ static NcclApi& nccl() {
     LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd) LOAD(GetErrorString) LOAD(AllReduce)
 #undef LOAD
     api.AlltoAll = reinterpret_cast<decltype(api.AlltoAll)>(dlsym(h, "ncclAlltoAll"));
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
     api.loaded = true;
   });
   return api;
@@ -133,10 +135,11 @@ struct LocalFabric {
   uint64_t generation = 0;
   bool aborted = false;
   double timeout_s = 600.0;
-  // per plan sequence number: each rank's staging pointer and events
+  // per plan sequence number: every rank's exchange buffers and events, per
+  // buffer set (a batched plan at p > 1 pipelines two sets)
   struct Slot {
-    std::vector<void*> staging, landing;
-    std::vector<cudaEvent_t> ready, done;
+    std::vector<void*> staging[2], landing[2];
+    std::vector<cudaEvent_t> ready[2], done[2];
   };
   // a deque: slot(seq) may grow it while other ranks hold references to
   // earlier slots (growing a deque at the end keeps references valid)
@@ -171,26 +174,57 @@ struct LocalFabric {
     aborted = true;
     cv.notify_all();
   }
-  Slot& slot(int seq) {
+  // publish this rank's buffers / events of one set (under the lock)
+  void publish(int seq, int rank, int set, void* stg, void* lnd, cudaEvent_t rdy, cudaEvent_t dn) {
     std::lock_guard<std::mutex> lk(mu);
     if ((int)slots.size() <= seq) slots.resize(seq + 1);
     Slot& s = slots[seq];
-    if ((int)s.staging.size() != p) {
-      s.staging.assign(p, nullptr);
-      s.landing.assign(p, nullptr);
-      s.ready.assign(p, nullptr);
-      s.done.assign(p, nullptr);
+    if ((int)s.staging[set].size() != p) {
+      s.staging[set].assign(p, nullptr);
+      s.landing[set].assign(p, nullptr);
+      s.ready[set].assign(p, nullptr);
+      s.done[set].assign(p, nullptr);
     }
-    return s;
+    s.staging[set][rank] = stg;
+    s.landing[set][rank] = lnd;
+    s.ready[set][rank] = rdy;
+    s.done[set][rank] = dn;
+  }
+  // copy every rank's entries of one set out (under the lock; call after a barrier)
+  void collect(int seq, int set, std::vector<void*>& stg, std::vector<void*>& lnd, std::vector<cudaEvent_t>& rdy,
+               std::vector<cudaEvent_t>& dn) {
+    std::lock_guard<std::mutex> lk(mu);
+    const Slot& s = slots[seq];
+    stg = s.staging[set];
+    lnd = s.landing[set];
+    rdy = s.ready[set];
+    dn = s.done[set];
   }
 };
 
+// transports of a communicator
+enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1, COMM_IPC = 2 };
+
 struct tffft_comm_s {
   int p = 1, rank = 0, device = 0;
-  bool is_nccl = false;
+  int kind = COMM_LOCAL;
+  bool is_nccl = false;  // kind == COMM_NCCL
   ncclComm_t nccl = nullptr;
-  std::shared_ptr<LocalFabric> fabric;
+  std::shared_ptr<LocalFabric> fabric;  // COMM_LOCAL
+  tffft_barrier_fn barrier_fn = nullptr;  // COMM_IPC: the caller's host barrier
+  void* barrier_ctx = nullptr;
+  bool aborted = false;
   int plan_seq = 0;
+  int barrier() {  // host barrier of the fabric kinds (local, IPC)
+    if (kind == COMM_LOCAL) return fabric->barrier();
+    if (aborted) return fail(TFFFT_ERR_TRANSPORT, "communicator aborted");
+    if (!barrier_fn) return fail(TFFFT_ERR_TRANSPORT, "IPC communicator without a barrier");
+    if (barrier_fn(barrier_ctx) != 0) {
+      aborted = true;
+      return fail(TFFFT_ERR_TRANSPORT, "IPC communicator: the host barrier failed");
+    }
+    return TFFFT_OK;
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -205,29 +239,49 @@ struct StageEvents {
 // created inside a timed region
 constexpr int kEventRing = 128;
 
+// One set of exchange buffers (p > 1).  Band q of every buffer is the
+// (n0/p, n1/p, n2c) block [q][i][j][k]; a batched plan pipelines two sets
+// (component c uses set c % 2) so component c's exchange overlaps component
+// c+1's stage 1.
+struct BufSet {
+  void* staging = nullptr;    // outgoing bands, staging[q] for rank q (pull / send-recv transports)
+  void* landing = nullptr;    // incoming bands, landing[s] from rank s; landing[rank] = the self band
+  void** band_dst = nullptr;  // device: destination block of each outgoing band (p pointers)
+  void** pull_ptrs = nullptr; // fabric pull: device list of (src, dst) per peer
+  // fabric transports (local, IPC): every rank's buffers and events of this set
+  std::vector<void*> peer_staging, peer_landing;
+  std::vector<cudaEvent_t> ready, done;  // [q]: rank q's "staging written" / "landing consumed"
+  bool own_events = false;
+};
+
 struct tffft_plan_s {
   tffft_comm_t comm = nullptr;
   int n0 = 0, n1 = 0, n2 = 0, p = 1, rank = 0, dtype = TFFFT_F64, pattern = TFFFT_PAIRWISE;
   int L0 = 0, L1 = 0, L2h = 0;
   int n0p = 0, n1p = 0, n2c = 0;
   size_t esz = 16;  // complex element bytes
+  int batch = 1;    // fields per forward / inverse call, back to back in memory
   int seq = 0;
-  void* staging = nullptr;   // outgoing peer bands [q][i][j][k]
-  void* landing = nullptr;   // incoming peer bands [q][i][j][k]
-  void** band_dst = nullptr; // device: destination block of each outgoing band (p pointers)
+  BufSet bs[2];
+  int nsets = 1;
+  int cur = 0;               // the set the stage launchers address
   bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
   bool peer_stores_wanted = false;  // NCCL communicator: peer stores once the peers' landing buffers are attached
-  std::vector<void*> peer_landing;  // NCCL + peer stores: rank q's landing buffer, opened through CUDA IPC
+  std::vector<void*> ipc_opened;    // peer mappings opened through CUDA IPC (closed at destroy)
+  std::vector<cudaEvent_t> ipc_events;  // peer events opened through CUDA IPC
   int* barrier_word = nullptr;      // NCCL + peer stores: one-int all-reduce used as a stream-ordered barrier
+  bool ipc_attached = false;        // IPC communicator: peers' buffers mapped
+  // batched p > 1: exchange stream and the pipeline's hand-off events per set
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_s1[2] = {nullptr, nullptr}, ev_x[2] = {nullptr, nullptr}, ev_s3[2] = {nullptr, nullptr};
   void* tw0 = nullptr;
   void* tw1 = nullptr;
   void* tw2 = nullptr;   // row pass tables (c2r, fused stage 1)
   void* tw2r = nullptr;  // row pass tables in the r2c kernel's schedule
   void* tw2c = nullptr;  // row pass tables in the c2r kernel's schedule
   void* tw2post = nullptr;
-  unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles)
+  unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles), batch * n0p planes
   double* row_stats = nullptr;          // per row records of the c2r kernel
-  void** pull_ptrs = nullptr;  // local fabric: device array [2 * nchunks] of (src, dst)
   // stage-3 four-step (fourstep.cuh): L2-resident scratch ring, counters, tables
   int fs_la = 0, fs_G = 0, fs_groups = 0;
   void* fs_scratch = nullptr;
@@ -404,11 +458,11 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
-// stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of the local slab
-static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int plane0 = 0, int nplanes = -1) {
-  if (nplanes < 0) nplanes = pl->n0p;
+// stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of `nplanes`
+// planes starting at `spec` (a batched p = 1 plan passes all batch * n0p planes)
+static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int nplanes) {
   ColParams c{};
-  c.data = static_cast<char*>(spec) + (size_t)plane0 * pl->n1 * pl->n2c * pl->esz;
+  c.data = spec;
   c.tw = pl->tw1;
   c.ncols = (long long)nplanes * pl->n2c;
   c.cpb = pl->n2c;
@@ -421,15 +475,18 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
   c.staging = nullptr;
   int rd = 0;
   if (pl->p > 1 && pl->strategy == 0) {
-    // forward epilogue: band q != rank -> band_dst[q] (staging[q], or rank q's landing[rank]);
-    // inverse: band q != rank is read from landing[q][i][j][k] (the exchange output)
-    c.staging = pl->landing;
-    c.band_dst = pl->band_dst;
+    // forward epilogue: band q -> band_dst[q] for EVERY q (the self band goes to
+    // landing[rank], peers to staging[q] or straight to rank q's landing);
+    // inverse: every band is read from landing[q][i][j][k] (the exchange output)
+    const BufSet& B = pl->bs[pl->cur];
+    c.staging = B.landing;
+    c.band_dst = B.band_dst;
+    c.self_band = -1;
     rd = inv ? 2 : 1;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
-    c.stg_base = (long long)plane0 * c.stg_grp;
+    c.stg_base = 0;
   }
 #if TFFFT_PROBES
   {  // profiling probe: every plane aliases plane 0 (same work, L2-resident footprint)
@@ -608,7 +665,7 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   if (pl->fs_la > 0) {
     FourStepParams f{};
     f.data = spec;
-    f.staging = (inv && pl->p > 1) ? pl->staging : nullptr;
+    f.staging = (inv && pl->p > 1) ? pl->bs[pl->cur].staging : nullptr;
     f.scratch = pl->fs_scratch;
     f.twA = pl->fs_twA;
     f.twB = pl->fs_twB;
@@ -628,18 +685,20 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     CUDA_TRY(fs_launch(pl, inv, pl->p == 1 ? 0 : (f.staging ? 3 : 2), f, s));
     return TFFFT_OK;
   }
+  const long long slab = (long long)pl->n0p * pl->n1 * pl->n2c;  // complex elements per field
+  const int nb = pl->p == 1 ? pl->batch : 1;  // p = 1: every field of the batch in one launch
   if (pl->p == 1) {
     bool done = false;
-    TRY(columns_tma(pl, pl->L0, inv, true, spec, (long long)pl->n1 * pl->n2c, 1, (long long)pl->n1 * pl->n2c, 0,
-                    pl->tw0, s, &done));
+    TRY(columns_tma(pl, pl->L0, inv, true, spec, (long long)pl->n1 * pl->n2c, nb, (long long)pl->n1 * pl->n2c,
+                    slab, pl->tw0, s, &done));
     if (done) return TFFFT_OK;
   }
   ColParams c{};
   c.data = spec;
   c.tw = pl->tw0;
-  c.ncols = (long long)pl->n1p * pl->n2c;
-  c.cpb = (int)std::min<long long>(c.ncols, 1LL << 30);
-  c.grp_stride = 0;
+  c.ncols = (long long)pl->n1p * pl->n2c * nb;
+  c.cpb = (int)std::min<long long>((long long)pl->n1p * pl->n2c, 1LL << 30);
+  c.grp_stride = slab;
   c.ic_shift = ilog2(pl->n0p);
   c.inner_stride = (long long)pl->n1 * pl->n2c;
   c.block_stride = (long long)pl->n1p * pl->n2c;
@@ -659,10 +718,13 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   }
   int rd = 0;
   if (pl->p > 1) {
-    // forward: block s != rank is read from landing[s][i][c] (the exchange output);
-    // inverse epilogue: block s != rank -> band_dst[s] (staging[s], or rank s's landing[rank])
-    c.staging = pl->landing;
-    c.band_dst = pl->band_dst;
+    // forward: block s is read from landing[s][i][c] (the exchange output; the
+    // self block from landing[rank]); inverse epilogue: block s -> band_dst[s]
+    // (landing[rank] for the self block, staging[s] or rank s's landing[rank])
+    const BufSet& B = pl->bs[pl->cur];
+    c.staging = B.landing;
+    c.band_dst = B.band_dst;
+    c.self_band = -1;
     rd = inv ? 1 : 2;
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = (long long)pl->n1p * pl->n2c;
@@ -672,19 +734,20 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   return TFFFT_OK;
 }
 
-static RowParams row_params(tffft_plan_t pl, void* real, void* spec, int plane0 = 0, int nplanes = -1) {
-  if (nplanes < 0) nplanes = pl->n0p;
-  const long long row0 = (long long)plane0 * pl->n1;
+// row pass over `nplanes` planes at (real, spec); the c2r statistics of those
+// rows go to the records of planes [stat_plane0, stat_plane0 + nplanes) (a
+// batch's planes are numbered field after field)
+static RowParams row_params(tffft_plan_t pl, void* real, void* spec, int nplanes, long long stat_plane0) {
   RowParams r{};
-  r.real = static_cast<char*>(real) + (size_t)row0 * pl->n2 * (pl->esz / 2);
-  r.spec = static_cast<char*>(spec) + (size_t)row0 * pl->n2c * pl->esz;
+  r.real = real;
+  r.spec = spec;
   r.tw = pl->tw2;
   r.tw_post = pl->tw2post;
   r.nrows = (long long)nplanes * pl->n1;
   r.n2c = pl->n2c;
   r.rows_per_plane = pl->n1;
   r.scale = 1.0 / ((double)pl->n0 * (double)pl->n1 * (double)pl->n2);
-  r.row_stats = pl->row_stats + 3 * row0;
+  r.row_stats = pl->row_stats + 3 * stat_plane0 * pl->n1;
   return r;
 }
 
@@ -693,7 +756,7 @@ static int stage1_fused(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaS
   Stage1Params f{};
   f.real = real;
   f.spec = spec;
-  f.staging = (fwd && pl->p > 1) ? pl->staging : nullptr;
+  f.staging = (fwd && pl->p > 1) ? pl->bs[pl->cur].staging : nullptr;
   f.tw_row = pl->tw2;
   f.tw_post = pl->tw2post;
   f.tw_col = pl->tw1;
@@ -724,11 +787,8 @@ static uint64_t wire_bytes(tffft_plan_t pl) {
   return (uint64_t)(pl->p - 1) * pl->n0p * pl->n1p * pl->n2c * pl->esz;
 }
 
-// all peers must have finished pulling from my staging before I overwrite it
-// Before this rank's epilogue writes its outgoing bands: in pull mode, every
-// peer must have finished pulling from our staging; with peer stores, every
-// peer must have finished reading its landing buffer (the host barrier makes
-// sure each peer recorded that event for the previous exchange).
+static size_t band_bytes(tffft_plan_t pl) { return (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz; }
+
 // Stream-ordered barrier over an NCCL communicator: a one-int all-reduce.  It
 // completes on this rank only after every rank's preceding kernels have
 // completed, so their peer stores into our landing buffer are visible (or,
@@ -740,48 +800,74 @@ static int nccl_barrier(tffft_plan_t pl, cudaStream_t s) {
   return TFFFT_OK;
 }
 
-static int fabric_guard_staging(tffft_plan_t pl, cudaStream_t s) {
+static bool fabric_kind(tffft_plan_t pl) { return pl->comm->kind != COMM_NCCL; }
+
+// Before a stage writes the outgoing bands of the current set.  Fabric pull
+// (local / IPC): every peer has finished pulling from our staging (its "done"
+// event of this set, recorded before the barrier that ended that exchange).
+// Peer stores: every peer has consumed its landing buffer -- the host barrier
+// makes sure each peer recorded that event for the previous exchange.  NCCL
+// send/recv needs nothing: the sends are stream-ordered before this stage.
+static int guard_outgoing(tffft_plan_t pl, cudaStream_t s) {
   if (pl->p == 1) return TFFFT_OK;
-  if (pl->comm->is_nccl) return pl->peer_stores ? nccl_barrier(pl, s) : TFFFT_OK;
-  auto& slot = pl->comm->fabric->slot(pl->seq);
-  if (pl->peer_stores) TRY(pl->comm->fabric->barrier());
+  BufSet& B = pl->bs[pl->cur];
+  if (!fabric_kind(pl)) return pl->peer_stores ? nccl_barrier(pl, s) : TFFFT_OK;
+  if (pl->peer_stores) TRY(pl->comm->barrier());
   for (int q = 0; q < pl->p; ++q)
-    if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.done[q], 0));
+    if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, B.done[q], 0));
   return TFFFT_OK;
 }
 
-// peer stores: this rank has consumed its landing buffer
-static int fabric_landing_consumed(tffft_plan_t pl, cudaStream_t s) {
-  if (!pl->peer_stores || pl->comm->is_nccl) return TFFFT_OK;  // NCCL: the next guard barrier covers it
-  CUDA_TRY(cudaEventRecord(pl->comm->fabric->slot(pl->seq).done[pl->rank], s));
+// peer stores: this rank has consumed its landing buffer of the current set
+static int landing_consumed(tffft_plan_t pl, cudaStream_t s) {
+  if (pl->p == 1 || !pl->peer_stores || !fabric_kind(pl)) return TFFFT_OK;  // NCCL: the next guard barrier covers it
+  CUDA_TRY(cudaEventRecord(pl->bs[pl->cur].done[pl->rank], s));
   return TFFFT_OK;
 }
 
-// destination block of each outgoing band for the write-redirect epilogues
-static int build_band_dst(tffft_plan_t pl) {
-  const size_t band = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
+// destination block of each outgoing band for the write-redirect epilogues of
+// one set.  The self band goes to landing[rank] (the next stage reads every
+// band from the landing buffer), except on NCCL COLLECTIVE without peer stores,
+// where it travels through the all-to-all's self slot (staging[rank] ->
+// landing[rank]).
+static int build_band_dst(tffft_plan_t pl, int set) {
+  BufSet& B = pl->bs[set];
+  const size_t band = band_bytes(pl);
   std::vector<void*> h(pl->p, nullptr);
+  const bool nccl_a2a = !fabric_kind(pl) && pl->pattern == TFFFT_COLLECTIVE && !pl->peer_stores && nccl().AlltoAll;
   for (int q = 0; q < pl->p; ++q) {
-    if (pl->peer_stores && pl->comm->is_nccl) {
-      h[q] = q == pl->rank ? static_cast<char*>(pl->staging) + (size_t)q * band
-                           : static_cast<char*>(pl->peer_landing[q]) + (size_t)pl->rank * band;
-    } else if (pl->peer_stores) {
-      auto& slot = pl->comm->fabric->slot(pl->seq);
-      h[q] = static_cast<char*>(slot.landing[q]) + (size_t)pl->rank * band;  // rank q's landing block for us
-    } else {
-      h[q] = static_cast<char*>(pl->staging) + (size_t)q * band;
-    }
+    if (q == pl->rank)
+      h[q] = static_cast<char*>(nccl_a2a ? B.staging : B.landing) + (size_t)q * band;
+    else if (pl->peer_stores)
+      h[q] = static_cast<char*>(B.peer_landing[q]) + (size_t)pl->rank * band;  // rank q's landing block for us
+    else
+      h[q] = static_cast<char*>(B.staging) + (size_t)q * band;
   }
-  if (!pl->band_dst) CUDA_TRY(cudaMalloc(&pl->band_dst, sizeof(void*) * pl->p));
-  CUDA_TRY(cudaMemcpy(pl->band_dst, h.data(), sizeof(void*) * pl->p, cudaMemcpyHostToDevice));
+  if (!B.band_dst) CUDA_TRY(cudaMalloc(&B.band_dst, sizeof(void*) * pl->p));
+  CUDA_TRY(cudaMemcpy(B.band_dst, h.data(), sizeof(void*) * pl->p, cudaMemcpyHostToDevice));
   return TFFFT_OK;
 }
 
-// The exchange proper (exchange.py:263-290): my staging band q (n0p chunks of
-// (n1/p)*n2c, contiguous) goes to rank q, whose landing band for me receives
-// it; the next FFT stage reads the landing buffer through the STRIDED_INPLACE
-// addressing, so no rearrangement pass follows.  One send and one receive per
-// peer (the reference posts one strided LayoutDescriptor per peer).
+// fabric pull list of one set, in the PAIRWISE ring order (d = 1 .. p-1: the
+// band of rank (rank - d) mod p): (peer's staging band for us, our landing band)
+static int build_pull_list(tffft_plan_t pl, int set) {
+  BufSet& B = pl->bs[set];
+  const size_t band = band_bytes(pl);
+  std::vector<void*> h;
+  for (int d = 1; d < pl->p; ++d) {
+    const int q = (pl->rank - d + pl->p) % pl->p;
+    h.push_back(static_cast<char*>(B.peer_staging[q]) + (size_t)pl->rank * band);
+    h.push_back(static_cast<char*>(B.landing) + (size_t)q * band);
+  }
+  if (!B.pull_ptrs) CUDA_TRY(cudaMalloc(&B.pull_ptrs, sizeof(void*) * 2 * (size_t)(pl->p - 1)));
+  CUDA_TRY(cudaMemcpy(B.pull_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  return TFFFT_OK;
+}
+
+// The exchange proper (exchange.py:263-290) of the current set: my band q
+// (n0p chunks of (n1/p)*n2c, contiguous in staging[q]) goes to rank q, whose
+// landing[rank] receives it; the next FFT stage reads the landing buffer
+// through the STRIDED_INPLACE addressing, so no rearrangement pass follows.
 // Failure detection: an asynchronous NCCL error (a peer died,
 // a network fault) surfaces as TFFFT_ERR_TRANSPORT on the next exchange, like
 // the reference fabric's abort propagation (transport.py:209-219, 446-467).
@@ -795,12 +881,26 @@ static int nccl_async_check(tffft_comm_t c) {
   return TFFFT_OK;
 }
 
-static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
-  (void)spec;
+static int launch_pull(tffft_plan_t pl, void* const* ptrs, int nchunks, cudaStream_t s) {
+  const long long bytes = (long long)band_bytes(pl);
+  const bool wide = bytes % 16 == 0;
+  const long long words = wide ? bytes / 16 : bytes / 8;
+  dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 2048), (unsigned)nchunks);
+  if (wide)
+    pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(ptrs, words, nchunks);
+  else
+    pull_chunks_kernel<int2><<<grid, 256, 0, s>>>(ptrs, words, nchunks);
+  pl->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return TFFFT_OK;
+}
+
+static int exchange(tffft_plan_t pl, cudaStream_t s) {
   if (pl->p == 1) return TFFFT_OK;
   TRY(nccl_async_check(pl->comm));
+  BufSet& B = pl->bs[pl->cur];
   const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
-  if (pl->peer_stores && pl->comm->is_nccl) {
+  if (pl->peer_stores && !fabric_kind(pl)) {
     // the epilogue already stored every band into its peer's landing buffer
     // over NVLink (CUDA IPC mapping): the exchange is the barrier
     TRY(nccl_barrier(pl, s));
@@ -810,25 +910,22 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
   if (pl->peer_stores) {
     // the epilogue already stored every band into its peer's landing buffer:
     // the exchange is the barrier after which every rank's stores are visible
-    LocalFabric& fab = *pl->comm->fabric;
-    auto& slot = fab.slot(pl->seq);
-    CUDA_TRY(cudaEventRecord(slot.ready[pl->rank], s));
-    TRY(fab.barrier());
+    CUDA_TRY(cudaEventRecord(B.ready[pl->rank], s));
+    TRY(pl->comm->barrier());
     for (int q = 0; q < pl->p; ++q)
-      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.ready[q], 0));
+      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, B.ready[q], 0));
     pl->counters[1] += wire_bytes(pl);
     return TFFFT_OK;
   }
-  if (pl->comm->is_nccl) {
+  if (!fabric_kind(pl)) {
     NcclApi& api = nccl();
     const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
-    char* stg = static_cast<char*>(pl->staging);
-    char* lnd = static_cast<char*>(pl->landing);
+    char* stg = static_cast<char*>(B.staging);
+    char* lnd = static_cast<char*>(B.landing);
     if (pl->pattern == TFFFT_COLLECTIVE && api.AlltoAll) {
       // COLLECTIVE (transport.py:395-419): every rank deposits all of its
-      // outgoing bands in one all-to-all.  Staging and landing hold p bands, so
-      // the self slot travels too (a local copy nobody reads: the self band
-      // stays in the slab).
+      // outgoing bands in one all-to-all; the self slot carries the self band
+      // from staging[rank] to landing[rank] (build_band_dst)
       NCCL_TRY(api.AlltoAll(stg, lnd, 2 * band, dt, pl->comm->nccl, s));
       pl->counters[1] += wire_bytes(pl);
       return TFFFT_OK;
@@ -841,58 +938,46 @@ static int exchange(tffft_plan_t pl, void* spec, cudaStream_t s) {
     }
     NCCL_TRY(api.GroupEnd());
   } else {
-    // the local fabric's pull is already collective-shaped for both patterns:
-    // every rank deposits (records its staging), waits for all p deposits,
-    // then collects its p-1 incoming bands in one launch
-    LocalFabric& fab = *pl->comm->fabric;
-    auto& slot = fab.slot(pl->seq);
-    CUDA_TRY(cudaEventRecord(slot.ready[pl->rank], s));
-    TRY(fab.barrier());
+    // fabric pull (local fabric or CUDA IPC across processes): every rank
+    // records that its staging is written, meets the others at the host
+    // barrier, then pulls its p-1 incoming bands from the peers' staging.
+    // PAIRWISE: one pull per peer in ring order (the reference posts one
+    // strided send/recv pair per peer); COLLECTIVE: all bands in one launch.
+    CUDA_TRY(cudaEventRecord(B.ready[pl->rank], s));
+    TRY(pl->comm->barrier());
     for (int q = 0; q < pl->p; ++q)
-      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, slot.ready[q], 0));
-    // pull: landing[q] <- staging_q[rank], one band per peer
-    const long long bytes = band * (long long)pl->esz;
-    const bool wide = bytes % 16 == 0;
-    const long long words = wide ? bytes / 16 : bytes / 8;
-    const int nchunks = pl->p - 1;
-    dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 2048), (unsigned)nchunks);
-    if (wide)
-      pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(pl->pull_ptrs, words, nchunks);
-    else
-      pull_chunks_kernel<int2><<<grid, 256, 0, s>>>(pl->pull_ptrs, words, nchunks);
-    pl->launches++;
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(slot.done[pl->rank], s));
-    TRY(fab.barrier());
+      if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, B.ready[q], 0));
+    if (pl->pattern == TFFFT_COLLECTIVE) {
+      TRY(launch_pull(pl, B.pull_ptrs, pl->p - 1, s));
+    } else {
+      for (int d = 1; d < pl->p; ++d) TRY(launch_pull(pl, B.pull_ptrs + 2 * (d - 1), 1, s));
+    }
+    CUDA_TRY(cudaEventRecord(B.done[pl->rank], s));
+    TRY(pl->comm->barrier());
   }
   pl->counters[1] += wire_bytes(pl);
   return TFFFT_OK;
 }
 
-// build the pull pointer list once all ranks registered their staging buffers
-static int fabric_setup(tffft_plan_t pl, void* /*unused*/) {
+// Local fabric: create this rank's events of every set, publish them with the
+// buffers, meet the other ranks and copy theirs (no reference into the shared
+// fabric is kept past the call).
+static int fabric_setup_local(tffft_plan_t pl) {
   LocalFabric& fab = *pl->comm->fabric;
-  auto& slot = fab.slot(pl->seq);
-  slot.staging[pl->rank] = pl->staging;
-  slot.landing[pl->rank] = pl->landing;
-  CUDA_TRY(cudaEventCreateWithFlags(&slot.ready[pl->rank], cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&slot.done[pl->rank], cudaEventDisableTiming));
-  TRY(fab.barrier());
-  return TFFFT_OK;
-}
-
-// pull list of the local fabric: (peer q's staging band for me, my landing band q)
-static int fabric_pull_list(tffft_plan_t pl) {
-  LocalFabric& fab = *pl->comm->fabric;
-  auto& slot = fab.slot(pl->seq);
-  const long long band = (long long)pl->n0p * pl->n1p * pl->n2c * (long long)pl->esz;
-  std::vector<void*> h;
-  for (int q = 0; q < pl->p; ++q) {
-    if (q == pl->rank) continue;
-    h.push_back(static_cast<char*>(slot.staging[q]) + (long long)pl->rank * band);
-    h.push_back(static_cast<char*>(pl->landing) + (long long)q * band);
+  for (int st = 0; st < pl->nsets; ++st) {
+    BufSet& B = pl->bs[st];
+    cudaEvent_t rdy, dn;
+    CUDA_TRY(cudaEventCreateWithFlags(&rdy, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&dn, cudaEventDisableTiming));
+    B.own_events = true;
+    fab.publish(pl->seq, pl->rank, st, B.staging, B.landing, rdy, dn);
   }
-  CUDA_TRY(cudaMemcpy(pl->pull_ptrs, h.data(), h.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  TRY(fab.barrier());
+  for (int st = 0; st < pl->nsets; ++st) {
+    BufSet& B = pl->bs[st];
+    fab.collect(pl->seq, st, B.peer_staging, B.peer_landing, B.ready, B.done);
+  }
+  TRY(fab.barrier());  // every rank has copied the table: the slot is never read again
   return TFFFT_OK;
 }
 
@@ -921,7 +1006,7 @@ static uint64_t offrank_block_bytes(tffft_plan_t pl) {
 static int pack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
   const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
   PermuteParams p{};
-  p.src = spec; p.src_self = spec; p.dst = pl->staging; p.self = -1;
+  p.src = spec; p.src_self = spec; p.dst = pl->bs[pl->cur].staging; p.self = -1;
   p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
   p.sa = n1p * n2c; p.sb = n2c; p.sc = (long long)pl->n1 * n2c;
   p.da = band; p.db = n0p * n2c; p.dc = n2c;
@@ -934,13 +1019,13 @@ static int pack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
 static int unpack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
   const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
   PermuteParams p{};
-  p.src = pl->p > 1 ? pl->landing : pl->staging;
+  p.src = pl->p > 1 ? pl->bs[pl->cur].landing : pl->bs[pl->cur].staging;
   p.dst = spec; p.self = pl->rank;
   p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
   p.sa = band; p.sb = n0p * n2c; p.sc = n2c;
   p.da = n0p * n2c; p.db = (long long)pl->n0 * n2c; p.dc = n2c;
   p.row_words = n2c;
-  p.src_self = pl->staging;  // indexed like the landing buffer: block `rank` of staging
+  p.src_self = pl->bs[pl->cur].staging;  // indexed like the landing buffer: block `rank` of staging
   TRY(permute(pl, p, s));
   pl->counters[2] += offrank_block_bytes(pl);
   return TFFFT_OK;
@@ -949,7 +1034,7 @@ static int unpack_forward(tffft_plan_t pl, void* spec, cudaStream_t s) {
 static int pack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
   const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
   PermuteParams p{};
-  p.src = spec; p.src_self = spec; p.dst = pl->staging; p.self = -1;
+  p.src = spec; p.src_self = spec; p.dst = pl->bs[pl->cur].staging; p.self = -1;
   p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
   p.sa = n0p * n2c; p.sb = (long long)pl->n0 * n2c; p.sc = n2c;
   p.da = band; p.db = n0p * n2c; p.dc = n2c;
@@ -962,8 +1047,8 @@ static int pack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
 static int unpack_inverse(tffft_plan_t pl, void* spec, cudaStream_t s) {
   const long long n2c = pl->n2c, n1p = pl->n1p, n0p = pl->n0p, band = n0p * n1p * n2c;
   PermuteParams p{};
-  p.src = pl->p > 1 ? pl->landing : pl->staging;
-  p.src_self = pl->staging;
+  p.src = pl->p > 1 ? pl->bs[pl->cur].landing : pl->bs[pl->cur].staging;
+  p.src_self = pl->bs[pl->cur].staging;
   p.dst = spec; p.self = pl->rank;
   p.A = pl->p; p.B = (int)n1p; p.C = (int)n0p;
   p.sa = band; p.sb = n0p * n2c; p.sc = n2c;
@@ -997,6 +1082,10 @@ static int stage3_flipped(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
   return TFFFT_OK;
 }
 
+struct PlanDeleter {
+  void operator()(tffft_plan_s* p) const { tffft_plan_destroy(p); }
+};
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1024,6 +1113,7 @@ int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tff
   c->rank = rank;
   c->device = device;
   c->is_nccl = true;
+  c->kind = COMM_NCCL;
   CUDA_TRY(cudaSetDevice(device));
   if (p > 1) {
     NcclApi& api = nccl();
@@ -1033,6 +1123,53 @@ int tffft_comm_init_rank(int p, int rank, const uint8_t id[128], int device, tff
     NCCL_TRY(api.CommInitRank(&c->nccl, p, uid, rank));
   }
   *comm = c.release();
+  return TFFFT_OK;
+}
+
+// single process, one communicator per listed device (ncclCommInitAll): the
+// run_spmd analogue across GPUs, one host thread driving each communicator
+int tffft_comm_init_all(int p, const int* devices, tffft_comm_t* comms) {
+  if (!comms || !devices) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (p < 1) return fail(TFFFT_ERR_CONFIGURATION, "communicator group needs p >= 1, got %d", p);
+  for (int a = 0; a < p; ++a)
+    for (int b = a + 1; b < p; ++b)
+      if (devices[a] == devices[b])
+        return fail(TFFFT_ERR_CONFIGURATION, "comm_init_all: device %d listed twice (NCCL needs one GPU per rank; "
+                    "use comm_init_local for ranks sharing a device)", devices[a]);
+  std::vector<ncclComm_t> nc(p, nullptr);
+  if (p > 1) {
+    NcclApi& api = nccl();
+    if (!api.loaded) return fail(TFFFT_ERR_TRANSPORT, "NCCL unavailable: %s", api.err.c_str());
+    if (!api.CommInitAll) return fail(TFFFT_ERR_TRANSPORT, "ncclCommInitAll missing from the loaded NCCL");
+    NCCL_TRY(api.CommInitAll(nc.data(), p, devices));
+  }
+  for (int r = 0; r < p; ++r) {
+    auto* c = new tffft_comm_s();
+    c->p = p;
+    c->rank = r;
+    c->device = devices[r];
+    c->is_nccl = true;
+    c->kind = COMM_NCCL;
+    c->nccl = nc[r];
+    comms[r] = c;
+  }
+  return TFFFT_OK;
+}
+
+// one process per rank, exchange through CUDA IPC mappings of the peers'
+// buffers ordered by IPC events, with the caller's host barrier (MPI, a
+// torch.distributed gloo group, ...) as the only host-side collective
+int tffft_comm_init_ipc(int p, int rank, int device, tffft_barrier_fn barrier, void* ctx, tffft_comm_t* comm) {
+  if (!comm || !barrier) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (p < 1 || rank < 0 || rank >= p) return fail(TFFFT_ERR_CONFIGURATION, "rank %d outside [0, %d)", rank, p);
+  auto* c = new tffft_comm_s();
+  c->p = p;
+  c->rank = rank;
+  c->device = device;
+  c->kind = COMM_IPC;
+  c->barrier_fn = barrier;
+  c->barrier_ctx = ctx;
+  *comm = c;
   return TFFFT_OK;
 }
 
@@ -1077,6 +1214,7 @@ int tffft_comm_device(tffft_comm_t c, int* d) {
 int tffft_comm_abort(tffft_comm_t c) {
   if (!c) return fail(TFFFT_ERR_CONFIGURATION, "null comm");
   if (c->fabric) c->fabric->abort();
+  c->aborted = true;
   if (c->nccl) {
     NCCL_TRY(nccl().CommAbort(c->nccl));
     c->nccl = nullptr;
@@ -1114,40 +1252,124 @@ int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   return TFFFT_OK;
 }
 
+// ---- CUDA IPC: export this rank's exchange buffers, attach the peers' -----
+// Blob of one plan: per buffer set, four 64-byte handles: staging memory,
+// landing memory, "ready" event, "done" event (events: IPC communicators only).
+static constexpr size_t kIpcSetBytes = 4 * 64;
+
+int tffft_plan_ipc_blob_bytes(tffft_plan_t pl, size_t* bytes) {
+  if (!pl || !bytes) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *bytes = (size_t)pl->nsets * kIpcSetBytes;
+  return TFFFT_OK;
+}
+
+int tffft_plan_ipc_export(tffft_plan_t pl, uint8_t* blob) {
+  if (!pl || !blob) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (pl->p == 1 || pl->comm->kind == COMM_LOCAL)
+    return fail(TFFFT_ERR_CONFIGURATION, "IPC handles exist for NCCL / IPC plans with p > 1 only");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64 && sizeof(cudaIpcEventHandle_t) == 64, "64-byte IPC handles");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  memset(blob, 0, (size_t)pl->nsets * kIpcSetBytes);
+  for (int st = 0; st < pl->nsets; ++st) {
+    BufSet& B = pl->bs[st];
+    uint8_t* o = blob + st * kIpcSetBytes;
+    cudaIpcMemHandle_t m;
+    CUDA_TRY(cudaIpcGetMemHandle(&m, B.staging));
+    memcpy(o, &m, 64);
+    CUDA_TRY(cudaIpcGetMemHandle(&m, B.landing));
+    memcpy(o + 64, &m, 64);
+    if (pl->comm->kind == COMM_IPC) {
+      cudaIpcEventHandle_t e;
+      CUDA_TRY(cudaIpcGetEventHandle(&e, B.ready[pl->rank]));
+      memcpy(o + 128, &e, 64);
+      CUDA_TRY(cudaIpcGetEventHandle(&e, B.done[pl->rank]));
+      memcpy(o + 192, &e, 64);
+    }
+  }
+  return TFFFT_OK;
+}
+
+// blobs: p blobs of tffft_plan_ipc_blob_bytes each, in rank order (all-gathered
+// by the caller).  Collective: every rank of the communicator must attach.
+// NCCL plans map the peers' landing buffers (peer stores, TFFFT_FLAG_PEER_STORES);
+// IPC plans map the peers' staging and landing buffers and open their events.
+int tffft_plan_ipc_attach(tffft_plan_t pl, const uint8_t* blobs) {
+  if (!pl || !blobs) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  if (pl->p == 1 || pl->comm->kind == COMM_LOCAL)
+    return fail(TFFFT_ERR_CONFIGURATION, "ipc_attach needs an NCCL or IPC plan with p > 1");
+  if (pl->comm->kind == COMM_NCCL && !pl->peer_stores_wanted)
+    return fail(TFFFT_ERR_CONFIGURATION, "ipc_attach on an NCCL plan needs TFFFT_FLAG_PEER_STORES");
+  if (pl->ipc_attached) return fail(TFFFT_ERR_PROTOCOL, "peers already attached");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  const size_t blob = (size_t)pl->nsets * kIpcSetBytes;
+  const bool ipc = pl->comm->kind == COMM_IPC;
+  for (int st = 0; st < pl->nsets; ++st) {
+    BufSet& B = pl->bs[st];
+    for (int q = 0; q < pl->p; ++q) {
+      if (q == pl->rank) continue;
+      const uint8_t* o = blobs + (size_t)q * blob + st * kIpcSetBytes;
+      cudaIpcMemHandle_t m;
+      if (ipc) {
+        memcpy(&m, o, 64);
+        CUDA_TRY(cudaIpcOpenMemHandle(&B.peer_staging[q], m, cudaIpcMemLazyEnablePeerAccess));
+        pl->ipc_opened.push_back(B.peer_staging[q]);
+      }
+      memcpy(&m, o + 64, 64);
+      CUDA_TRY(cudaIpcOpenMemHandle(&B.peer_landing[q], m, cudaIpcMemLazyEnablePeerAccess));
+      pl->ipc_opened.push_back(B.peer_landing[q]);
+      if (ipc) {
+        cudaIpcEventHandle_t e;
+        memcpy(&e, o + 128, 64);
+        CUDA_TRY(cudaIpcOpenEventHandle(&B.ready[q], e));
+        pl->ipc_events.push_back(B.ready[q]);
+        memcpy(&e, o + 192, 64);
+        CUDA_TRY(cudaIpcOpenEventHandle(&B.done[q], e));
+        pl->ipc_events.push_back(B.done[q]);
+      }
+    }
+  }
+  if (!ipc) {
+    CUDA_TRY(cudaMalloc(&pl->barrier_word, sizeof(int)));
+    CUDA_TRY(cudaMemset(pl->barrier_word, 0, sizeof(int)));
+  }
+  pl->peer_stores = pl->peer_stores_wanted;
+  pl->ipc_attached = true;
+  for (int st = 0; st < pl->nsets; ++st) {
+    if (ipc) TRY(build_pull_list(pl, st));
+    TRY(build_band_dst(pl, st));
+  }
+  return TFFFT_OK;
+}
+
+// round-1 names of the NCCL peer-store attach (one buffer set): the landing
+// handle alone, and p landing handles in rank order
 int tffft_plan_landing_handle(tffft_plan_t pl, uint8_t handle[64]) {
   if (!pl || !handle) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
-  if (!pl->comm->is_nccl || pl->p == 1 || !pl->landing)
-    return fail(TFFFT_ERR_CONFIGURATION, "landing handles exist for NCCL plans with p > 1 only");
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
-  CUDA_TRY(cudaSetDevice(pl->comm->device));
-  cudaIpcMemHandle_t h;
-  CUDA_TRY(cudaIpcGetMemHandle(&h, pl->landing));
-  memcpy(handle, &h, 64);
+  if (pl->comm->kind != COMM_NCCL || pl->p == 1 || pl->nsets != 1)
+    return fail(TFFFT_ERR_CONFIGURATION, "landing handles exist for unbatched NCCL plans with p > 1 only");
+  uint8_t blob[kIpcSetBytes];
+  TRY(tffft_plan_ipc_export(pl, blob));
+  memcpy(handle, blob + 64, 64);
   return TFFFT_OK;
 }
 
 int tffft_plan_attach_peers(tffft_plan_t pl, const uint8_t* handles) {
   if (!pl || !handles) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
-  if (!pl->comm->is_nccl || pl->p == 1 || !pl->peer_stores_wanted)
-    return fail(TFFFT_ERR_CONFIGURATION, "attach_peers needs an NCCL plan with p > 1 created with TFFFT_FLAG_PEER_STORES");
-  if (pl->peer_stores) return fail(TFFFT_ERR_PROTOCOL, "peers already attached");
-  CUDA_TRY(cudaSetDevice(pl->comm->device));
-  pl->peer_landing.assign(pl->p, nullptr);
-  for (int q = 0; q < pl->p; ++q) {
-    if (q == pl->rank) { pl->peer_landing[q] = pl->landing; continue; }
-    cudaIpcMemHandle_t h;
-    memcpy(&h, handles + 64 * (size_t)q, 64);
-    CUDA_TRY(cudaIpcOpenMemHandle(&pl->peer_landing[q], h, cudaIpcMemLazyEnablePeerAccess));
-  }
-  CUDA_TRY(cudaMalloc(&pl->barrier_word, sizeof(int)));
-  CUDA_TRY(cudaMemset(pl->barrier_word, 0, sizeof(int)));
-  pl->peer_stores = true;
-  TRY(build_band_dst(pl));
-  return TFFFT_OK;
+  if (pl->comm->kind != COMM_NCCL || pl->p == 1 || pl->nsets != 1 || !pl->peer_stores_wanted)
+    return fail(TFFFT_ERR_CONFIGURATION,
+                "attach_peers needs an unbatched NCCL plan with p > 1 created with TFFFT_FLAG_PEER_STORES");
+  std::vector<uint8_t> blobs((size_t)pl->p * kIpcSetBytes, 0);
+  for (int q = 0; q < pl->p; ++q) memcpy(blobs.data() + (size_t)q * kIpcSetBytes + 64, handles + 64 * (size_t)q, 64);
+  return tffft_plan_ipc_attach(pl, blobs.data());
 }
 
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,
                          tffft_plan_t* out) {
+  return tffft_plan_create_batched(n0, n1, n2, dtype, pattern, flags, 1, comm, out);
+}
+
+int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, int flags, int batch,
+                              tffft_comm_t comm, tffft_plan_t* out) {
   // TMA column passes: explicit flag = every supported pass; environment
   // defaults = the measured winner (float32 column passes, profiles/r01s2/tma_cols.txt, r01s6/f32_stage1b_tma.txt)
   // unless TFFFT_TMA_COLS says otherwise
@@ -1179,14 +1401,19 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
                 (long long)(n0 / p) * n1 * (n2 / 2 + 1));
   if (pattern != TFFFT_PAIRWISE && pattern != TFFFT_COLLECTIVE)
     return fail(TFFFT_ERR_CONFIGURATION, "unknown comm pattern %d", pattern);
+  if (batch < 1) return fail(TFFFT_ERR_CONFIGURATION, "batch must be >= 1, got %d", batch);
+  if (p == 1 && (long long)batch * (n0 / p) * n1 * (n2 / 2 + 1) >= (1LL << 32))
+    return fail(TFFFT_ERR_SIZE, "a p = 1 batch of %d fields exceeds 2^32 complex elements per launch", batch);
 
-  auto pl = std::make_unique<tffft_plan_s>();
+  // a failed create releases what it allocated (PlanDeleter -> tffft_plan_destroy)
+  std::unique_ptr<tffft_plan_s, PlanDeleter> pl(new tffft_plan_s());
   pl->comm = comm;
   pl->n0 = n0; pl->n1 = n1; pl->n2 = n2;
   pl->p = p; pl->rank = comm->rank; pl->dtype = dtype; pl->pattern = pattern;
   pl->L0 = ilog2(n0); pl->L1 = ilog2(n1); pl->L2h = ilog2(n2) - 1;
   pl->n0p = n0 / p; pl->n1p = n1 / p; pl->n2c = n2 / 2 + 1;
   pl->esz = dtype == TFFFT_F64 ? 16 : 8;
+  pl->batch = batch;
   pl->strategy = strategy;
   pl->tma_cols = (p == 1 && strategy == 0) ? tma_cols : 0;
   CUDA_TRY(cudaSetDevice(comm->device));
@@ -1199,33 +1426,63 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
   TRY(upload_table(pass_table(pl->L2h, c2r_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2c, &ws));
   TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
   CUDA_TRY(cudaMalloc(&pl->col_ticket, sizeof(unsigned long long)));
-  CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * pl->n0p));
-  CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p));
-  ws += sizeof(unsigned long long) * 3 * pl->n0p;
-  CUDA_TRY(cudaMalloc(&pl->row_stats, sizeof(double) * 3 * (size_t)pl->n0p * pl->n1));
-  ws += sizeof(double) * 3 * (size_t)pl->n0p * pl->n1;
+  const size_t planes = (size_t)batch * pl->n0p;  // statistics records: every plane of the batch
+  CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * planes));
+  CUDA_TRY(cudaMemset(pl->stats, 0, sizeof(unsigned long long) * 3 * planes));
+  ws += sizeof(unsigned long long) * 3 * planes;
+  CUDA_TRY(cudaMalloc(&pl->row_stats, sizeof(double) * 3 * planes * pl->n1));
+  ws += sizeof(double) * 3 * planes * pl->n1;
   if (p == 1 && strategy == 1) {  // TRANSPOSE packs even on one rank (exchange.py:195-219)
     const size_t sb = (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz;
-    CUDA_TRY(cudaMalloc(&pl->staging, sb));
+    CUDA_TRY(cudaMalloc(&pl->bs[0].staging, sb));
     ws += sb;
   }
   if (p > 1) {
+    // a batched plan pipelines two buffer sets (component c's exchange runs on
+    // the exchange stream while component c+1's stage 1 fills the other set)
+    pl->nsets = (batch > 1 && strategy == 0) ? 2 : 1;
     const size_t sb = (size_t)p * pl->n0p * pl->n1p * pl->n2c * pl->esz;
-    CUDA_TRY(cudaMalloc(&pl->staging, sb));
-    CUDA_TRY(cudaMalloc(&pl->landing, sb));
-    ws += 2 * sb;
-    if (comm->is_nccl) {
-      pl->peer_stores_wanted = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
-    } else {
-      const size_t nptr = 2 * (size_t)(p - 1);
-      CUDA_TRY(cudaMalloc(&pl->pull_ptrs, nptr * sizeof(void*)));
-      ws += nptr * sizeof(void*);
-      pl->seq = comm->plan_seq++;
-      pl->peer_stores = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
-      TRY(fabric_setup(pl.get(), nullptr));
-      TRY(fabric_pull_list(pl.get()));
+    const unsigned evflags = cudaEventDisableTiming | (comm->kind == COMM_IPC ? cudaEventInterprocess : 0);
+    for (int st = 0; st < pl->nsets; ++st) {
+      BufSet& B = pl->bs[st];
+      CUDA_TRY(cudaMalloc(&B.staging, sb));
+      CUDA_TRY(cudaMalloc(&B.landing, sb));
+      ws += 2 * sb;
+      B.peer_staging.assign(p, nullptr);
+      B.peer_landing.assign(p, nullptr);
+      B.peer_staging[pl->rank] = B.staging;
+      B.peer_landing[pl->rank] = B.landing;
+      if (comm->kind == COMM_IPC) {  // events other processes open through cudaIpcOpenEventHandle
+        B.ready.assign(p, nullptr);
+        B.done.assign(p, nullptr);
+        CUDA_TRY(cudaEventCreateWithFlags(&B.ready[pl->rank], evflags));
+        CUDA_TRY(cudaEventCreateWithFlags(&B.done[pl->rank], evflags));
+        B.own_events = true;
+      }
     }
-    TRY(build_band_dst(pl.get()));
+    if (pl->nsets > 1) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&pl->xstream, cudaStreamNonBlocking));
+      for (int st = 0; st < 2; ++st) {
+        CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_s1[st], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_x[st], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_s3[st], cudaEventDisableTiming));
+      }
+    }
+    const bool ps = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
+    if (comm->kind == COMM_LOCAL) {
+      pl->seq = comm->plan_seq++;
+      pl->peer_stores = ps;
+      TRY(fabric_setup_local(pl.get()));
+      for (int st = 0; st < pl->nsets; ++st) {
+        TRY(build_pull_list(pl.get(), st));
+        TRY(build_band_dst(pl.get(), st));
+      }
+    } else {
+      // NCCL: peer stores once tffft_plan_ipc_attach mapped the peers' landing
+      // buffers; IPC: the exchange needs the attach (peers' staging, landing, events)
+      pl->peer_stores_wanted = ps;
+      for (int st = 0; st < pl->nsets; ++st) TRY(build_band_dst(pl.get(), st));
+    }
   }
   // stage 3 as an L2-resident four-step when the n0 columns are long (fourstep.cuh)
   {
@@ -1234,7 +1491,7 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // element than the direct 8-column kernel, which is faster today; opt-in
     // with TFFFT_FOURSTEP=1.
     // optional schedules are single-rank kernels (no staging / landing addressing)
-    const int la = ((flags & TFFFT_FLAG_FOURSTEP_STAGE3) && p == 1 && strategy == 0) ? fourstep_la(pl->L0) : 0;
+    const int la = ((flags & TFFFT_FLAG_FOURSTEP_STAGE3) && p == 1 && strategy == 0 && batch == 1) ? fourstep_la(pl->L0) : 0;
     if (la > 0) {
       static const char* env_g = getenv("TFFFT_FS_G");
       const long long ncols = (long long)pl->n1p * pl->n2c;
@@ -1257,7 +1514,8 @@ int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int fla
     // measured at 1024^3 (profiles/r01_*): the fused persistent stage 1 keeps the
     // planes in L2 but its mixed row/column tasks run at lower occupancy; the two
     // streaming kernels are faster today, so fusion is opt-in (TFFFT_FUSE=1)
-    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && p == 1 && strategy == 0 && stage1_fused_supported(pl->L2h, pl->L1)) {
+    if ((flags & TFFFT_FLAG_FUSED_STAGE1) && p == 1 && strategy == 0 && batch == 1 &&
+        stage1_fused_supported(pl->L2h, pl->L1)) {
       pl->s1_fused = true;
       CUDA_TRY(cudaMalloc(&pl->s1_counters, sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p)));
       ws += sizeof(unsigned) * (1 + 2 * (size_t)pl->n0p);
@@ -1308,16 +1566,30 @@ static int harvest(tffft_plan_t pl, StageEvents& ev) {
 int tffft_plan_destroy(tffft_plan_t pl) {
   if (!pl) return TFFFT_OK;
   cudaSetDevice(pl->comm->device);
+  if (pl->xstream) cudaStreamSynchronize(pl->xstream);
   free_events(pl);
   cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2c); cudaFree(pl->tw2post);
-  cudaFree(pl->stats); cudaFree(pl->row_stats); cudaFree(pl->staging); cudaFree(pl->landing); cudaFree(pl->pull_ptrs);
-  cudaFree(pl->band_dst);
+  cudaFree(pl->stats); cudaFree(pl->row_stats);
+  for (void* m : pl->ipc_opened) cudaIpcCloseMemHandle(m);
+  for (cudaEvent_t e : pl->ipc_events) cudaEventDestroy(e);
+  for (auto& B : pl->bs) {
+    cudaFree(B.staging); cudaFree(B.landing); cudaFree(B.pull_ptrs); cudaFree(B.band_dst);
+    if (B.own_events && !B.ready.empty()) {
+      // own events (the local fabric's peers' entries belong to the peers' plans)
+      if (B.ready[pl->rank]) cudaEventDestroy(B.ready[pl->rank]);
+      if (B.done[pl->rank]) cudaEventDestroy(B.done[pl->rank]);
+    }
+  }
+  for (int st = 0; st < 2; ++st) {
+    if (pl->ev_s1[st]) cudaEventDestroy(pl->ev_s1[st]);
+    if (pl->ev_x[st]) cudaEventDestroy(pl->ev_x[st]);
+    if (pl->ev_s3[st]) cudaEventDestroy(pl->ev_s3[st]);
+  }
+  if (pl->xstream) cudaStreamDestroy(pl->xstream);
   cudaFree(pl->fs_scratch); cudaFree(pl->fs_counters); cudaFree(pl->fs_twA); cudaFree(pl->fs_twB);
   cudaFree(pl->fs_twN);
   cudaFree(pl->s1_counters);
   cudaFree(pl->col_ticket);
-  for (size_t q = 0; q < pl->peer_landing.size(); ++q)
-    if (pl->peer_landing[q] && (int)q != pl->rank) cudaIpcCloseMemHandle(pl->peer_landing[q]);
   cudaFree(pl->barrier_word);
   delete pl;
   return TFFFT_OK;
@@ -1361,96 +1633,217 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
-int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* stream) {
-  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
-  TRY(check_ptr(real_in, "real_in", pl->esz));
-  TRY(check_ptr(spec_out, "spec_out", pl->esz));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaSetDevice(pl->comm->device));
-  NvtxRange call("tffft.forward");
-  StageEvents* ev;
-  TRY(begin_events(pl, true, s, &ev));
-  {  // stage 1: planes (dfft.py:161-163)
-    NvtxRange r("stage1");
-    TRY(fabric_guard_staging(pl, s));
-    if (pl->s1_fused) {
-      TRY(stage1_fused(pl, const_cast<void*>(real_in), spec_out, true, s));
-    } else {
-      CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real_in), spec_out), s));
-      TRY(stage1_columns(pl, spec_out, false, s));
-    }
-  }
+// ---- orchestration ---------------------------------------------------------
+static size_t real_bytes(tffft_plan_t pl) { return (size_t)pl->n0p * pl->n1 * pl->n2 * (pl->esz / 2); }
+static size_t spec_bytes(tffft_plan_t pl) { return (size_t)pl->n0p * pl->n1 * pl->n2c * pl->esz; }
+
+static int check_ready(tffft_plan_t pl) {
+  if (pl->p > 1 && pl->comm->kind == COMM_IPC && !pl->ipc_attached)
+    return fail(TFFFT_ERR_PROTOCOL, "IPC plan used before tffft_plan_ipc_attach");
+  if (pl->comm->aborted) return fail(TFFFT_ERR_TRANSPORT, "communicator aborted");
+  return TFFFT_OK;
+}
+
+// stage 1 (dfft.py:161-163) of `nf` fields at (real, spec): r2c rows + n1 columns
+static int fwd_stage1(tffft_plan_t pl, const void* real, void* spec, int nf, cudaStream_t s) {
+  NvtxRange r("stage1");
+  if (pl->s1_fused) return stage1_fused(pl, const_cast<void*>(real), spec, true, s);
+  CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real), spec, nf * pl->n0p, 0), s));
+  return stage1_columns(pl, spec, false, s, nf * pl->n0p);
+}
+// stage 1' (dfft.py:206-209) of one field (component c of the batch) or, at
+// p = 1, of `nf` fields: n1 columns + c2r rows with 1/(n0 n1 n2)
+static int inv_stage1(tffft_plan_t pl, void* spec, void* real, int nf, int c, cudaStream_t s) {
+  NvtxRange r("stage1");
+  if (pl->s1_fused) return stage1_fused(pl, real, spec, false, s);
+  TRY(stage1_columns(pl, spec, true, s, nf * pl->n0p));
+  TRY(landing_consumed(pl, s));
+  CUDA_TRY(c2r_launch(pl, row_params(pl, real, spec, nf * pl->n0p, (long long)c * pl->n0p), s));
+  return TFFFT_OK;
+}
+
+static int forward_field(tffft_plan_t pl, const void* real, void* spec, int nf, cudaStream_t s, StageEvents* ev) {
+  TRY(guard_outgoing(pl, s));
+  TRY(fwd_stage1(pl, real, spec, nf, s));
   MARK(ev, 1, s);
   if (pl->strategy == 1) {
     // TRANSPOSE (exchange.py:195-219): pack -> contiguous exchange -> unpack
-    TRY(pack_forward(pl, spec_out, s));
-    TRY(exchange(pl, spec_out, s));
-    TRY(unpack_forward(pl, spec_out, s));
+    TRY(pack_forward(pl, spec, s));
+    TRY(exchange(pl, s));
+    TRY(unpack_forward(pl, spec, s));
     MARK(ev, 2, s);
-    TRY(stage3_flipped(pl, spec_out, false, s));
+    TRY(stage3_flipped(pl, spec, false, s));
     MARK(ev, 3, s);
     return TFFFT_OK;
   }
   {  // exchange (exchange.py:263-276)
     NvtxRange r("exchange");
-    TRY(exchange(pl, spec_out, s));
+    TRY(exchange(pl, s));
   }
   MARK(ev, 2, s);
   {  // stage 3: strided columns (dfft.py:170-171)
     NvtxRange r("stage3");
-    TRY(stage3_columns(pl, spec_out, false, s));
-    TRY(fabric_landing_consumed(pl, s));
+    TRY(stage3_columns(pl, spec, false, s));
+    TRY(landing_consumed(pl, s));
   }
   MARK(ev, 3, s);
   return TFFFT_OK;
 }
 
-int tffft_inverse(tffft_plan_t pl, void* spec, void* real_out, void* stream) {
-  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
-  TRY(check_ptr(spec, "spec_inout", pl->esz));
-  TRY(check_ptr(real_out, "real_out", pl->esz));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  CUDA_TRY(cudaSetDevice(pl->comm->device));
-  NvtxRange call("tffft.inverse");
-  StageEvents* ev;
-  TRY(begin_events(pl, false, s, &ev));
+static int inverse_field(tffft_plan_t pl, void* spec, void* real, int nf, int c, cudaStream_t s, StageEvents* ev) {
   if (pl->s1_fused)  // the fused kernel max-reduces into the per-plane statistics
     CUDA_TRY(cudaMemsetAsync(pl->stats, 0, sizeof(unsigned long long) * 3 * pl->n0p, s));
-  // stage 3' (dfft.py:196-197)
-  TRY(fabric_guard_staging(pl, s));
+  TRY(guard_outgoing(pl, s));
   if (pl->strategy == 1) {
     TRY(stage3_flipped(pl, spec, true, s));
     MARK(ev, 1, s);
     // TRANSPOSE (exchange.py:222-260): pack -> contiguous exchange -> un-transpose
     TRY(pack_inverse(pl, spec, s));
-    TRY(exchange(pl, spec, s));
+    TRY(exchange(pl, s));
     TRY(unpack_inverse(pl, spec, s));
     MARK(ev, 2, s);
   } else {
-    {
+    {  // stage 3' (dfft.py:196-197)
       NvtxRange r("stage3");
       TRY(stage3_columns(pl, spec, true, s));
     }
     MARK(ev, 1, s);
     {  // exchange (exchange.py:279-290)
       NvtxRange r("exchange");
-      TRY(exchange(pl, spec, s));
+      TRY(exchange(pl, s));
     }
     MARK(ev, 2, s);
   }
-  {  // stage 1' (dfft.py:206-209)
-    NvtxRange r("stage1");
-    if (pl->s1_fused) {
-      TRY(stage1_fused(pl, real_out, spec, false, s));
-    } else {
-      TRY(stage1_columns(pl, spec, true, s));
-      TRY(fabric_landing_consumed(pl, s));
-      CUDA_TRY(c2r_launch(pl, row_params(pl, real_out, spec), s));
+  TRY(inv_stage1(pl, spec, real, nf, c, s));
+  MARK(ev, 3, s);
+  return TFFFT_OK;
+}
+
+// Batched p > 1 (STRIDED): a two-deep software pipeline over the fields.  The
+// stages run on the caller's stream s, the exchanges on the plan's exchange
+// stream x; field c uses buffer set c % 2, so field c's exchange overlaps
+// field c+1's producing stage.  Enqueue order on s:
+//   produce(0), produce(1), consume(0), produce(2), consume(1), ...
+// Hand-offs: x waits produce(c) (ev_s1); consume(c) waits exchange(c) (ev_x);
+// produce(c+2) reuses the set after exchange(c) read its staging (ev_x).
+// Every rank enqueues in the same order, so the fabric's host barriers and
+// NCCL's per-communicator ordering see the same sequence on every rank.
+extern "C++" {
+template <class Produce, class Consume>
+static int pipeline(tffft_plan_t pl, cudaStream_t s, Produce produce, Consume consume) {
+  cudaStream_t x = pl->xstream;
+  const int B = pl->batch;
+  for (int c = 0; c <= B; ++c) {
+    if (c < B) {
+      const int st = c & 1;
+      pl->cur = st;
+      if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[st], 0));
+      TRY(guard_outgoing(pl, s));
+      TRY(produce(c));
+      CUDA_TRY(cudaEventRecord(pl->ev_s1[st], s));
+      CUDA_TRY(cudaStreamWaitEvent(x, pl->ev_s1[st], 0));
+      {
+        NvtxRange r("exchange");
+        TRY(exchange(pl, x));
+      }
+      CUDA_TRY(cudaEventRecord(pl->ev_x[st], x));
+    }
+    if (c >= 1) {
+      const int st = (c - 1) & 1;
+      pl->cur = st;
+      CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[st], 0));
+      TRY(consume(c - 1));
+      CUDA_TRY(cudaEventRecord(pl->ev_s3[st], s));
     }
   }
+  pl->cur = 0;
+  return TFFFT_OK;
+}
+
+}  // extern "C++"
+
+int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* stream) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  TRY(check_ptr(real_in, "real_in", pl->esz));
+  TRY(check_ptr(spec_out, "spec_out", pl->esz));
+  TRY(check_ready(pl));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  NvtxRange call("tffft.forward");
+  const char* real = static_cast<const char*>(real_in);
+  char* spec = static_cast<char*>(spec_out);
+  if (pl->p == 1 && pl->strategy == 0) {  // every field of the batch in the same launches
+    StageEvents* ev;
+    TRY(begin_events(pl, true, s, &ev));
+    return forward_field(pl, real, spec, pl->batch, s, ev);
+  }
+  if (pl->nsets == 1) {  // one field at a time
+    for (int c = 0; c < pl->batch; ++c) {
+      StageEvents* ev;
+      TRY(begin_events(pl, true, s, &ev));
+      pl->cur = 0;
+      TRY(forward_field(pl, real + c * real_bytes(pl), spec + c * spec_bytes(pl), 1, s, ev));
+    }
+    return TFFFT_OK;
+  }
+  StageEvents* ev;  // pipelined: the whole call is timed as stage 1 + stage 3
+  TRY(begin_events(pl, true, s, &ev));
+  MARK(ev, 1, s);
+  MARK(ev, 2, s);
+  TRY(pipeline(
+      pl, s, [&](int c) { return fwd_stage1(pl, real + c * real_bytes(pl), spec + c * spec_bytes(pl), 1, s); },
+      [&](int c) {
+        NvtxRange r("stage3");
+        TRY(stage3_columns(pl, spec + c * spec_bytes(pl), false, s));
+        return landing_consumed(pl, s);
+      }));
   MARK(ev, 3, s);
+  return TFFFT_OK;
+}
+
+int tffft_inverse(tffft_plan_t pl, void* spec_inout, void* real_out, void* stream) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  TRY(check_ptr(spec_inout, "spec_inout", pl->esz));
+  TRY(check_ptr(real_out, "real_out", pl->esz));
+  TRY(check_ready(pl));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  NvtxRange call("tffft.inverse");
+  char* spec = static_cast<char*>(spec_inout);
+  char* real = static_cast<char*>(real_out);
+  if (pl->p == 1 && pl->strategy == 0) {
+    StageEvents* ev;
+    TRY(begin_events(pl, false, s, &ev));
+    TRY(inverse_field(pl, spec, real, pl->batch, 0, s, ev));
+  } else if (pl->nsets == 1) {
+    for (int c = 0; c < pl->batch; ++c) {
+      StageEvents* ev;
+      TRY(begin_events(pl, false, s, &ev));
+      pl->cur = 0;
+      TRY(inverse_field(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), 1, c, s, ev));
+    }
+  } else {
+    StageEvents* ev;
+    TRY(begin_events(pl, false, s, &ev));
+    MARK(ev, 1, s);
+    MARK(ev, 2, s);
+    TRY(pipeline(
+        pl, s,
+        [&](int c) {
+          NvtxRange r("stage3");
+          return stage3_columns(pl, spec + c * spec_bytes(pl), true, s);
+        },
+        [&](int c) { return inv_stage1(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), 1, c, s); }));
+    MARK(ev, 3, s);
+  }
   pl->last_inverse_stream = s;
   pl->inverse_ran = true;
+  return TFFFT_OK;
+}
+
+int tffft_plan_batch(tffft_plan_t pl, int* batch) {
+  if (!pl || !batch) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *batch = pl->batch;
   return TFFFT_OK;
 }
 
@@ -1500,17 +1893,18 @@ int tffft_consistency(tffft_plan_t pl, double* residue) {
   if (!pl->inverse_ran) return TFFFT_OK;
   CUDA_TRY(cudaSetDevice(pl->comm->device));
   if (!pl->s1_fused) {  // fold the c2r row records into per-plane maxima
-    reduce_row_stats_kernel<<<pl->n0p, 256, 0, pl->last_inverse_stream>>>(pl->row_stats, pl->n1, pl->stats);
+    reduce_row_stats_kernel<<<pl->n0p * pl->batch, 256, 0, pl->last_inverse_stream>>>(pl->row_stats, pl->n1, pl->stats);
     pl->launches++;
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaStreamSynchronize(pl->last_inverse_stream));
-  std::vector<double> st(3 * (size_t)pl->n0p);
+  const int planes = pl->n0p * pl->batch;  // every plane of the batch, field after field
+  std::vector<double> st(3 * (size_t)planes);
   CUDA_TRY(cudaMemcpy(st.data(), pl->stats, st.size() * sizeof(double), cudaMemcpyDeviceToHost));
   double res = 0.0;
   int bad = -1;
   double bad_v = 0.0, bad_tol = 0.0;
-  for (int i = 0; i < pl->n0p; ++i) {
+  for (int i = 0; i < planes; ++i) {
     // kernels.py:222-223 (C2R_RESIDUE_TOL = 1e-9, calibrated for float64); float32
     // plans use 1e-4, which still flags an O(1) imaginary DC / Nyquist bin
     const double rtol = pl->dtype == TFFFT_F64 ? 1e-9 : 1e-4;
@@ -1526,8 +1920,8 @@ int tffft_consistency(tffft_plan_t pl, double* residue) {
   *residue = res;
   if (bad >= 0)
     return fail(TFFFT_ERR_CONSISTENCY,
-                "bins 0 and n/2 must be real for a half spectrum (plane %d: imag %.3e > %.3e)", bad, bad_v,
-                bad_tol);
+                "bins 0 and n/2 must be real for a half spectrum (field %d, plane %d: imag %.3e > %.3e)",
+                bad / pl->n0p, bad % pl->n0p, bad_v, bad_tol);
   return TFFFT_OK;
 }
 

@@ -23,8 +23,8 @@ from .exchange import Strategy
 from .layout import DistAxis, GlobalGrid, RealSlab, SlabLayout, SpectralSlab, SpectralTag, validate
 from .transport import CommPattern, CopyCounter, Endpoint
 
-__all__ = ["FftPlan", "plan", "forward", "inverse", "gather_spectral", "scatter_real",
-           "gather_real", "scatter_spectral", "DTYPES"]
+__all__ = ["FftPlan", "plan", "forward", "inverse", "forward_many", "inverse_many", "gather_spectral",
+           "scatter_real", "gather_real", "scatter_spectral", "DTYPES"]
 
 # precision name -> (C enum, real torch dtype, complex torch dtype)
 DTYPES = {
@@ -45,9 +45,10 @@ class FftPlan:
     spectral_layout: SlabLayout
     dtype: str
     handle: ctypes.c_void_p
-    work1: torch.Tensor      # spectral slab, plan-owned (forward output)
-    real_out: torch.Tensor   # real slab, plan-owned (inverse output)
+    work1: torch.Tensor      # spectral slab(s), plan-owned (forward output); batch slabs back to back
+    real_out: torch.Tensor   # real slab(s), plan-owned (inverse output); batch slabs back to back
     check_consistency: bool = True
+    batch: int = 1
     last_imag_residue: float = 0.0
     _timing: bool = field(default=False, repr=False)
 
@@ -128,15 +129,22 @@ def _spectral_tag(strategy: Strategy) -> SpectralTag:
 
 def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED,
          comm_pattern: CommPattern = CommPattern.PAIRWISE, dtype: str = "float64",
-         check_consistency: bool = True, algorithms: tuple[str, ...] | None = None) -> FftPlan:
-    """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric.
+         check_consistency: bool = True, algorithms: tuple[str, ...] | None = None,
+         batch: int = 1) -> FftPlan:
+    """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric, and on
+    NCCL (peer stores) / IPC communicators, whose buffers are exchanged here.
 
     ``algorithms`` selects optional kernel schedules ("fused_stage1",
     "fourstep_stage3", "peer_stores", "tma_columns"); None takes the library
     defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS environment
     switches; by default the 512- and 1024-point column passes at p = 1 are
-    TMA-fed)."""
+    TMA-fed).  ``batch`` > 1 makes a batched plan: ``forward_many`` /
+    ``inverse_many`` transform ``batch`` fields per call (one launch per stage
+    over all fields at p = 1; field c's exchange overlapping field c+1's
+    compute at p > 1)."""
     validate(grid, comm.p)
+    if not isinstance(batch, int) or batch < 1:
+        raise ConfigurationError(f"batch must be a positive int, got {batch!r}")
     if not isinstance(comm_pattern, CommPattern):
         raise ConfigurationError(f"comm_pattern must be a CommPattern, got {comm_pattern!r}")
     if dtype not in DTYPES:
@@ -152,26 +160,31 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
         flags = (0 if flags < 0 else flags) | TRANSPOSE_FLAG
     h = ctypes.c_void_p()
     with torch.cuda.device(comm.device):
-        _lib.check(_lib.lib().tffft_plan_create_ex(grid.n0, grid.n1, grid.n2, code, _PATTERN_CODE[comm_pattern], flags, comm.handle,
-                                                   ctypes.byref(h)))
+        _lib.check(_lib.lib().tffft_plan_create_batched(grid.n0, grid.n1, grid.n2, code, _PATTERN_CODE[comm_pattern],
+                                                        flags, batch, comm.handle, ctypes.byref(h)))
         p, rank = comm.p, comm.rank
         dev = torch.device("cuda", comm.device)
-        work1 = torch.empty((grid.n0 // p) * grid.n1 * grid.n2c, dtype=cdt, device=dev)
-        real_out = torch.empty((grid.n0 // p) * grid.n1 * grid.n2, dtype=rdt, device=dev)
-    if comm.kind == "nccl" and comm.p > 1 and (flags >= 0 and flags & ALGORITHM_FLAGS["peer_stores"]):
-        # fused exchange over NVLink: map every peer's landing buffer (CUDA IPC)
-        from .transport import allgather_handles
-        buf = ctypes.create_string_buffer(64)
-        _lib.check(_lib.lib().tffft_plan_landing_handle(h, buf))
-        allh = allgather_handles(buf.raw, comm.rank, comm.p)
+        work1 = torch.empty(batch * (grid.n0 // p) * grid.n1 * grid.n2c, dtype=cdt, device=dev)
+        real_out = torch.empty(batch * (grid.n0 // p) * grid.n1 * grid.n2, dtype=rdt, device=dev)
+    peer_stores = flags >= 0 and bool(flags & ALGORITHM_FLAGS["peer_stores"])
+    if comm.p > 1 and (comm.kind == "ipc" or (comm.kind == "nccl" and peer_stores)):
+        # CUDA IPC: every rank exports its exchange buffers (and, on an IPC
+        # communicator, its events); the blobs are all-gathered in rank order
+        # and each rank maps the peers' (fused exchange over NVLink for NCCL)
+        n = ctypes.c_size_t()
+        _lib.check(_lib.lib().tffft_plan_ipc_blob_bytes(h, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
         with torch.cuda.device(comm.device):
-            _lib.check(_lib.lib().tffft_plan_attach_peers(h, allh))
+            _lib.check(_lib.lib().tffft_plan_ipc_export(h, buf))
+        allh = comm.allgather_bytes(buf.raw)
+        with torch.cuda.device(comm.device):
+            _lib.check(_lib.lib().tffft_plan_ipc_attach(h, allh))
     return FftPlan(
         grid=grid, comm=comm, strategy=strategy, comm_pattern=comm_pattern,
         real_layout=SlabLayout(grid, p, rank, DistAxis.REAL_AXIS0),
         spectral_layout=SlabLayout(grid, p, rank, DistAxis.SPECTRAL_AXIS1),
         dtype=dtype, handle=h, work1=work1, real_out=real_out,
-        check_consistency=check_consistency,
+        check_consistency=check_consistency, batch=batch,
     )
 
 
@@ -196,6 +209,8 @@ def forward(fp: FftPlan, real: RealSlab, out: torch.Tensor | None = None) -> Spe
     STRIDED_INPLACE (Strategy.STRIDED) or CONTIGUOUS_FLIPPED
     (Strategy.TRANSPOSE).  The result is backed by plan memory unless ``out``
     is given."""
+    if fp.batch != 1:
+        raise ContractError(f"plan has batch={fp.batch}: use forward_many")
     if real.layout != fp.real_layout:
         raise ContractError(f"slab layout {real.layout} does not match plan {fp.real_layout}")
     _, rdt, cdt = DTYPES[fp.dtype]
@@ -215,6 +230,8 @@ def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) ->
     Collective; consumes ``spec`` in place.  With ``fp.check_consistency`` the
     call synchronises and raises ConsistencyError for a non-Hermitian half
     spectrum, as the reference's _c2r_rows does (kernels.py:223-238)."""
+    if fp.batch != 1:
+        raise ContractError(f"plan has batch={fp.batch}: use inverse_many")
     expected = _spectral_tag(fp.strategy)
     if spec.tag is not expected:
         raise ContractError(f"plan strategy {fp.strategy} expects a {expected} slab, got {spec.tag}")
@@ -229,11 +246,57 @@ def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) ->
     _lib.check(_lib.lib().tffft_inverse(fp.handle, ctypes.c_void_p(spec.data.data_ptr()),
                                         ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
     if fp.check_consistency:
-        res = ctypes.c_double()
-        status = _lib.lib().tffft_consistency(fp.handle, ctypes.byref(res))
-        fp.last_imag_residue = max(fp.last_imag_residue, float(res.value))
-        _lib.check(status)
+        _check_consistency(fp)
     return RealSlab(fp.real_layout, dst)
+
+
+def _check_consistency(fp: FftPlan) -> None:
+    res = ctypes.c_double()
+    status = _lib.lib().tffft_consistency(fp.handle, ctypes.byref(res))
+    fp.last_imag_residue = max(fp.last_imag_residue, float(res.value))
+    _lib.check(status)
+
+
+def forward_many(fp: FftPlan, real: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Forward r2c of ``fp.batch`` fields in one call (batched plan).
+
+    ``real`` holds the fields' real slabs back to back (``batch`` x
+    n0/p*n1*n2 elements, e.g. a (batch, slab) tensor); returns their
+    STRIDED_INPLACE spectral slabs back to back (plan memory unless ``out``)."""
+    _, rdt, cdt = DTYPES[fp.dtype]
+    if fp.strategy is not Strategy.STRIDED:
+        raise ContractError("forward_many runs the STRIDED strategy")
+    _check_tensor(real, fp, rdt, "real slabs")
+    if real.numel() != fp.real_out.numel():
+        raise ContractError(f"real slabs need {fp.real_out.numel()} elements ({fp.batch} fields), got {real.numel()}")
+    dst = fp.work1 if out is None else out
+    _check_tensor(dst, fp, cdt, "spectral output")
+    if dst.numel() != fp.work1.numel():
+        raise ContractError(f"spectral output needs {fp.work1.numel()} elements, got {dst.numel()}")
+    _lib.check(_lib.lib().tffft_forward(fp.handle, ctypes.c_void_p(real.data_ptr()),
+                                        ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
+    return dst
+
+
+def inverse_many(fp: FftPlan, spec: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Inverse c2r of ``fp.batch`` fields in one call (batched plan); consumes
+    ``spec`` (the fields' spectral slabs back to back).  The Hermitian
+    consistency check runs once for the whole batch."""
+    _, rdt, cdt = DTYPES[fp.dtype]
+    if fp.strategy is not Strategy.STRIDED:
+        raise ContractError("inverse_many runs the STRIDED strategy")
+    _check_tensor(spec, fp, cdt, "spectral slabs")
+    if spec.numel() != fp.work1.numel():
+        raise ContractError(f"spectral slabs need {fp.work1.numel()} elements ({fp.batch} fields), got {spec.numel()}")
+    dst = fp.real_out if out is None else out
+    _check_tensor(dst, fp, rdt, "real output")
+    if dst.numel() != fp.real_out.numel():
+        raise ContractError(f"real output needs {fp.real_out.numel()} elements, got {dst.numel()}")
+    _lib.check(_lib.lib().tffft_inverse(fp.handle, ctypes.c_void_p(spec.data_ptr()),
+                                        ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
+    if fp.check_consistency:
+        _check_consistency(fp)
+    return dst
 
 
 # ---------------------------------------------------------------------------

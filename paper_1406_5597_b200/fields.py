@@ -17,10 +17,11 @@ import math
 
 import torch
 
-from .dfft import DTYPES, FftPlan, forward, inverse
+from .dfft import DTYPES, FftPlan, forward, forward_many, inverse, inverse_many
+from .errors import ContractError
 from .layout import RealSlab, SpectralSlab, SpectralTag
 
-__all__ = ["radial_wavenumber", "turbulence_spectrum", "forward_batch", "inverse_batch"]
+__all__ = ["radial_wavenumber", "turbulence_spectrum", "turbulence_spectra", "forward_batch", "inverse_batch"]
 
 
 def radial_wavenumber(fp: FftPlan, dtype=torch.float64) -> torch.Tensor:
@@ -42,26 +43,78 @@ def radial_wavenumber(fp: FftPlan, dtype=torch.float64) -> torch.Tensor:
     return torch.sqrt(k2).reshape(-1)
 
 
+def _amplitude(fp: FftPlan, kmin: float, kmax: float, exponent: float) -> torch.Tensor:
+    kr = radial_wavenumber(fp)
+    shell = (kr >= kmin) & (kr <= kmax)
+    ksafe = torch.where(shell, kr, torch.ones_like(kr))
+    amp = torch.where(shell, torch.sqrt(ksafe ** exponent / (4.0 * math.pi * ksafe ** 2)), torch.zeros_like(kr))
+    return amp.to(DTYPES[fp.dtype][1])
+
+
 def turbulence_spectrum(fp: FftPlan, noise: RealSlab, kmin: float = 1.0, kmax: float = 340.0,
                         exponent: float = -5.0 / 3.0, out: torch.Tensor | None = None) -> SpectralSlab:
     """Collective.  ``noise`` is this rank's slab of a real white-noise field
     (any seeded generator); returns the shaped spectrum (forward of the noise
     times the radial amplitude), backed by ``out`` or plan memory."""
     spec = forward(fp, noise, out=out)
-    kr = radial_wavenumber(fp)
-    shell = (kr >= kmin) & (kr <= kmax)
-    ksafe = torch.where(shell, kr, torch.ones_like(kr))
-    amp = torch.where(shell, torch.sqrt(ksafe ** exponent / (4.0 * math.pi * ksafe ** 2)), torch.zeros_like(kr))
-    rdt = DTYPES[fp.dtype][1]
-    spec.data.mul_(amp.to(rdt))
+    spec.data.mul_(_amplitude(fp, kmin, kmax, exponent))
     return SpectralSlab(fp.spectral_layout, SpectralTag.STRIDED_INPLACE, spec.data)
 
 
-def inverse_batch(fp: FftPlan, specs: list[SpectralSlab], outs: list[torch.Tensor]) -> list[RealSlab]:
-    """Batched inverse c2r of several components with one plan (consumes specs)."""
-    return [inverse(fp, s, out=o) for s, o in zip(specs, outs)]
+def turbulence_spectra(fp: FftPlan, noise: torch.Tensor, kmin: float = 1.0, kmax: float = 340.0,
+                       exponent: float = -5.0 / 3.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Batched plan: ``noise`` holds ``fp.batch`` white-noise real slabs back
+    to back; returns the ``fp.batch`` shaped spectra back to back."""
+    spec = forward_many(fp, noise, out=out)
+    spec.view(fp.batch, -1).mul_(_amplitude(fp, kmin, kmax, exponent))
+    return spec
 
 
-def forward_batch(fp: FftPlan, reals: list[RealSlab], outs: list[torch.Tensor]) -> list[SpectralSlab]:
-    """Batched forward r2c of several components with one plan."""
-    return [forward(fp, r, out=o) for r, o in zip(reals, outs)]
+def _contiguous_run(ts: list[torch.Tensor]) -> torch.Tensor | None:
+    """The one tensor the list is a back-to-back run of, or None."""
+    base, n = ts[0], ts[0].numel()
+    step = n * base.element_size()
+    for i, t in enumerate(ts):
+        if t.numel() != n or not t.is_contiguous() or t.data_ptr() != base.data_ptr() + i * step:
+            return None
+    return torch.as_strided(base, (len(ts) * n,), (1,))
+
+
+def inverse_batch(fp: FftPlan, specs: list, outs: list[torch.Tensor] | None = None) -> list[RealSlab]:
+    """Inverse c2r of several fields (consumes specs).  A batched plan
+    (``fp.batch == len(specs)``) runs them in one library call -- one launch
+    per stage at p = 1, exchange/compute overlap at p > 1 -- when the spectra
+    are back-to-back views of one buffer (else they are gathered first)."""
+    data = [s.data if isinstance(s, SpectralSlab) else s for s in specs]
+    if fp.batch == 1:
+        outs = outs or [None] * len(data)
+        return [inverse(fp, SpectralSlab(fp.spectral_layout, SpectralTag.STRIDED_INPLACE, d), out=o)
+                for d, o in zip(data, outs)]
+    if len(data) != fp.batch:
+        raise ContractError(f"plan has batch={fp.batch}, got {len(data)} fields")
+    run = _contiguous_run(data)
+    if run is None:
+        run = torch.cat([d.reshape(-1) for d in data])
+    dst = None if outs is None else _contiguous_run(outs)
+    if outs is not None and dst is None:
+        raise ContractError("outputs must be back-to-back views of one buffer")
+    res = inverse_many(fp, run, out=dst).view(fp.batch, -1)
+    return [RealSlab(fp.real_layout, res[c]) for c in range(fp.batch)]
+
+
+def forward_batch(fp: FftPlan, reals: list, outs: list[torch.Tensor] | None = None) -> list[SpectralSlab]:
+    """Forward r2c of several fields (see inverse_batch)."""
+    data = [r.data if isinstance(r, RealSlab) else r for r in reals]
+    if fp.batch == 1:
+        outs = outs or [None] * len(data)
+        return [forward(fp, RealSlab(fp.real_layout, d), out=o) for d, o in zip(data, outs)]
+    if len(data) != fp.batch:
+        raise ContractError(f"plan has batch={fp.batch}, got {len(data)} fields")
+    run = _contiguous_run(data)
+    if run is None:
+        run = torch.cat([d.reshape(-1) for d in data])
+    dst = None if outs is None else _contiguous_run(outs)
+    if outs is not None and dst is None:
+        raise ContractError("outputs must be back-to-back views of one buffer")
+    res = forward_many(fp, run, out=dst).view(fp.batch, -1)
+    return [SpectralSlab(fp.spectral_layout, SpectralTag.STRIDED_INPLACE, res[c]) for c in range(fp.batch)]

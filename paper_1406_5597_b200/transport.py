@@ -1,14 +1,24 @@
 """Communicators for the GPU exchange (mirror of slabfft.transport's public
 surface, reference pkg/src/slabfft/transport.py:35-43, 425-468).
 
-Two backends behind one ``Endpoint``:
+Three transports behind one ``Endpoint``:
 
 LOCAL   p endpoints share an in-process fabric on ONE device; each rank is
         driven by its own host thread (the reference's run_spmd model,
-        transport.py:433-468).  The exchange is a device-side pull of peer
-        chunks straight into the vacated STRIDED_INPLACE bands.
-NCCL    one process per GPU (torchrun); grouped ncclSend/ncclRecv over
-        NVLink/NVSwitch, chunk-granular landing in the same layout.
+        transport.py:433-468).  The exchange is a device-side pull of every
+        peer's staging band into this rank's landing buffer.
+NCCL    one GPU per rank over NVLink/NVSwitch: one process per GPU (torchrun,
+        ``init_nccl_endpoint``) or one process driving all of them
+        (``make_communicators(p, devices=[...])``, ncclCommInitAll, one host
+        thread per rank).  Grouped ncclSend/ncclRecv (PAIRWISE) or one
+        ncclAlltoAll (COLLECTIVE) from the staging bands into the landing bands.
+IPC     one process per rank, any device assignment (several processes may
+        share a GPU): the plan's staging / landing buffers and events are
+        exchanged as CUDA IPC handles; the exchange is the LOCAL fabric's pull
+        across processes, with a torch.distributed (gloo) group as the host
+        barrier (``init_ipc_endpoint``).
+In every transport the FFT stage after the exchange reads the landing bands
+through the STRIDED_INPLACE addressing: no unpack pass.
 """
 
 from __future__ import annotations
@@ -31,6 +41,7 @@ __all__ = [
     "make_communicators",
     "run_spmd",
     "init_nccl_endpoint",
+    "init_ipc_endpoint",
     "allgather_handles",
 ]
 
@@ -70,13 +81,15 @@ class Endpoint:
     """One rank's handle on the exchange fabric."""
 
     def __init__(self, handle: int, rank: int, p: int, device: int, kind: str,
-                 host_barrier: threading.Barrier | None = None):
+                 host_barrier: threading.Barrier | None = None, group=None, keepalive=None):
         self._handle = ctypes.c_void_p(handle)
         self.rank = rank
         self.p = p
         self.device = device
         self.kind = kind
         self._host_barrier = host_barrier
+        self._group = group            # torch.distributed group of an IPC endpoint
+        self._keepalive = keepalive    # the ctypes barrier callback of an IPC endpoint
         self._closed = False
 
     @property
@@ -94,8 +107,17 @@ class Endpoint:
                     self._host_barrier.wait(timeout=600)
                 except threading.BrokenBarrierError as exc:
                     raise TransportError("fabric aborted while waiting at barrier") from exc
+        elif self.kind == "ipc" and self.p > 1:
+            torch.distributed.barrier(group=self._group)
         elif self.p > 1 and torch.distributed.is_initialized():
             torch.distributed.barrier()
+
+    def allgather_bytes(self, blob: bytes) -> bytes:
+        """Every rank's equal-sized blob, concatenated in rank order (the
+        CUDA IPC handle exchange of NCCL peer-store and IPC plans)."""
+        if self.kind == "ipc":
+            return _allgather(blob, self.rank, self.p, self._group)
+        return allgather_handles(blob, self.rank, self.p)
 
     def check(self) -> None:
         """Raise TransportError if the communicator failed asynchronously
@@ -114,11 +136,19 @@ class Endpoint:
 
 
 def make_communicators(p: int, mode: CommMode = CommMode.THREADED, device: int | None = None,
-                       timeout: float = 600.0) -> list[Endpoint]:
-    """p connected endpoints sharing one in-process fabric on one GPU
-    (transport.py:425-430)."""
+                       timeout: float = 600.0, devices: list[int] | None = None) -> list[Endpoint]:
+    """p connected endpoints (transport.py:425-430): sharing one in-process
+    fabric on one GPU, or -- with ``devices`` (one distinct GPU per rank) --
+    NCCL communicators created together by this process (ncclCommInitAll)."""
     if p < 1:
         raise ConfigurationError(f"communicator group needs p >= 1, got {p}")
+    if devices is not None:
+        devs = [int(d) for d in devices]
+        if len(devs) != p:
+            raise ConfigurationError(f"need {p} devices, got {len(devs)}")
+        arr = (ctypes.c_void_p * p)()
+        _lib.check(_lib.lib().tffft_comm_init_all(p, (ctypes.c_int * p)(*devs), arr))
+        return [Endpoint(arr[r], r, p, devs[r], "nccl") for r in range(p)]
     dev = torch.cuda.current_device() if device is None else int(device)
     arr = (ctypes.c_void_p * p)()
     _lib.check(_lib.lib().tffft_comm_init_local(p, dev, arr))
@@ -127,18 +157,17 @@ def make_communicators(p: int, mode: CommMode = CommMode.THREADED, device: int |
 
 
 def run_spmd(p: int, fn, mode: CommMode = CommMode.THREADED, device: int | None = None,
-             timeout: float = 600.0) -> list:
+             timeout: float = 600.0, devices: list[int] | None = None) -> list:
     """Run fn(endpoint) on p ranks (one host thread each) and return the
     results in rank order; the first failure aborts the fabric and is
-    re-raised (transport.py:433-468)."""
-    eps = make_communicators(p, mode, device, timeout)
+    re-raised (transport.py:433-468).  ``devices``: one GPU per rank (NCCL)."""
+    eps = make_communicators(p, mode, device, timeout, devices=devices)
     results: list = [None] * p
     errors: list[BaseException | None] = [None] * p
-    dev = eps[0].device
 
     def body(rank: int) -> None:
         try:
-            torch.cuda.set_device(dev)
+            torch.cuda.set_device(eps[rank].device)
             results[rank] = fn(eps[rank])
         except BaseException as exc:  # noqa: BLE001 - re-raised below
             errors[rank] = exc
@@ -181,6 +210,42 @@ def init_nccl_endpoint(device: int | None = None) -> Endpoint:
     h = ctypes.c_void_p()
     _lib.check(_lib.lib().tffft_comm_init_rank(p, rank, bytes(uid), dev, ctypes.byref(h)))
     return Endpoint(h.value, rank, p, dev, "nccl")
+
+
+def init_ipc_endpoint(device: int | None = None, group=None) -> Endpoint:
+    """Endpoint for this process of a torch.distributed job whose exchange runs
+    over CUDA IPC (any backend for ``group``, gloo included): the group's
+    barrier is the library's host barrier, and plans all-gather their IPC
+    handles over it.  Ranks may share a GPU."""
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise ConfigurationError("torch.distributed is not initialised")
+    rank, p = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device() if device is None else int(device)
+
+    def _barrier(_ctx) -> int:
+        try:
+            dist.barrier(group=group)
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the library as a transport failure
+            return 1
+
+    cb = _lib.BARRIER_FN(_barrier)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib().tffft_comm_init_ipc(p, rank, dev, ctypes.cast(cb, ctypes.c_void_p), None,
+                                              ctypes.byref(h)))
+    return Endpoint(h.value, rank, p, dev, "ipc", group=group, keepalive=cb)
+
+
+def _allgather(blob: bytes, rank: int, p: int, group) -> bytes:
+    import torch.distributed as dist
+
+    got: list = [None] * p
+    dist.all_gather_object(got, bytes(blob), group=group)
+    if {len(b) for b in got} != {len(blob)}:
+        raise TransportError(f"handle sizes differ across ranks: {sorted({len(b) for b in got})}")
+    return b"".join(got)
 
 
 def allgather_handles(handle: bytes, rank: int, p: int) -> bytes:
