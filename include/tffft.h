@@ -81,6 +81,8 @@ int tffft_comm_init_all(int p, const int* devices, tffft_comm_t* comms);
  * events; `barrier` is the only host-side collective (MPI, a gloo group, ...).
  * Ranks may share a device (several processes on one GPU) or not (P2P). */
 int tffft_comm_init_ipc(int p, int rank, int device, tffft_barrier_fn barrier, void* ctx, tffft_comm_t* comm);
+/* host barrier of a local-fabric or IPC communicator (TFFFT_ERR_CONFIGURATION on NCCL) */
+int tffft_comm_barrier(tffft_comm_t comm);
 /* asynchronous communicator failure (ncclCommGetAsyncError) as TFFFT_ERR_TRANSPORT;
  * TFFFT_OK for a healthy or local communicator (transport.py:209-219 abort propagation) */
 int tffft_comm_check(tffft_comm_t comm);

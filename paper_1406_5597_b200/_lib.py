@@ -26,6 +26,7 @@ _SIGS = {
     "tffft_comm_init_ipc": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p,
                                        _c.POINTER(_c.c_void_p)]),
     "tffft_comm_check": (_c.c_int, [_c.c_void_p]),
+    "tffft_comm_barrier": (_c.c_int, [_c.c_void_p]),
     "tffft_comm_rank": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_comm_size": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_comm_device": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),

@@ -19,11 +19,26 @@
 // the end of a group are zero-filled by the load and never stored.  Results
 // are bit-identical to col_fft_kernel's (same engine, same twiddles).
 //
-// Measured on 1024^3 (profiles/r01s2/tma_cols.txt): float32 stage 3 (16-column
-// tiles, 512 threads) 2.29 -> 1.78 ms per launch; float64 unchanged (3.69 vs
-// 3.75 ms stage 3, 3.26 vs 3.27 ms stage 1b), so float64 keeps col_fft_kernel.
-// Storing half of each tile through the TMA unit as well (staged behind the
-// next tile's boxes in the exchange buffer) did not change either.
+// Two-level addressing (p > 1, template TWO and the 4D load mode): the rows
+// of a STRIDED_INPLACE column are n0/p planes x p blocks, and the landing
+// buffer holds block s of every column at landing[s][i][c].  Loads then go
+// through a 4D map (cols, rows_in, rows_out, groups) -- row r is (r mod rows_in,
+// r / rows_in) -- in boxes that never cross a block; stores go through a table
+// of up to kTmaTab block pointers: element r of column c of group g lands at
+// tab[r >> sin_shift] + g * sgstride + c + (r mod 2^sin_shift) * sin_stride.
+// That is the forward stage-3 read of the landing bands and in-place write,
+// the inverse stage-3' write-redirect of every block (self block to
+// landing[rank], peers to staging or straight into the peer's landing
+// buffer), the forward stage-1b write-redirect and the inverse stage-1b' read
+// of the landing bands -- the reference's strided exchange datatype
+// (exchange.py:114-121) applied by the FFT's own TMA boxes and stores.
+//
+// Measured on 1024^3 (profiles/r01s10/tma_f64_ticket.txt, r01s11/tma_512.txt):
+// with the ticket tile order the TMA kernel is the default for every 512- and
+// 1024-point column pass of either precision (2.96 ms per float64 1024^3
+// launch against 3.25-3.69 ms for col_fft_kernel).  Storing half of each tile
+// through the TMA unit as well (staged behind the next tile's boxes in the
+// exchange buffer) did not change the time.
 #pragma once
 #include <cuda.h>
 
@@ -58,6 +73,8 @@ struct TmaColCfg {
                              B * sizeof(cx<T>) <= 256 && (NBOX == 1 || 2 * NPF == NBOX) && SH::TPT % 2 == 0;
 };
 
+constexpr int kTmaTab = 16;  // block pointers of the two-level stores (p <= 16)
+
 struct TmaColParams {
   void* data;            // column base (element 0 of group 0, column 0)
   const void* tw;        // pass tables (fft_engine.cuh layout)
@@ -71,9 +88,16 @@ struct TmaColParams {
   int parity;            // rows 8 bytes off 16-byte alignment on odd rows: even rows through `map`, odd
                          // rows through `map_odd`, whose boxes start on the aligned address before the
                          // row segment and are one complex wider on each side (pitch B + 2, data at +1)
+  int load4;             // 4D map (2*cols, rows_in, rows_out, groups): row r at (r mod rows_in, r >> lin_shift)
+  int lin_shift;         // log2(rows_in)
+  int brows;             // rows per box in the 4D mode (<= rows_in, <= 256)
+  int sin_shift;         // TWO stores: log2(rows per table block)
+  long long sin_stride;  // TWO stores: elements between the rows of a block
+  long long sgstride;    // TWO stores: elements between groups
+  void* tab[kTmaTab];    // TWO stores: block base pointers
 };
 
-template <typename T, int L, bool INV, bool WIDE>
+template <typename T, int L, bool INV, bool WIDE, bool TWO>
 __global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, 1)
 col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_odd,
                const TmaColParams prm) {
@@ -138,6 +162,12 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     const int pitch = (prm.parity && h) ? B + 2 : B;
     mbar_arrive_tx(bar + h, (unsigned)(sizeof(cx<T>) * (size_t)BOX * pitch * (q1 - q0)));
     cx<T>* dst = h ? xb : pf;
+    if (prm.load4) {  // two-level rows: boxes of brows rows, never across a block
+      const int r0 = q0 * BOX, r1 = q1 * BOX, rmask = (1 << prm.lin_shift) - 1;
+      for (int r = r0; r < r1; r += prm.brows)
+        tma_load4(dst + (size_t)(r - r0) * B, &map, 2 * c0, r & rmask, r >> prm.lin_shift, grp, bar + h, pol);
+      return;
+    }
     for (int q = q0; q < q1; ++q) {
       if (prm.parity)
         tma_load3(dst + (size_t)(q - q0) * BOX * pitch, h ? &map_odd : &map, 2 * c0, (q - q0) * BOX, grp, bar + h,
@@ -176,7 +206,18 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     ST::finish(xs, v, tt, b, s_tw, hook);
     int grp, c0;
     coords(cur, grp, c0);
-    if (c0 + b < prm.cols) {
+    if (TWO && c0 + b < prm.cols) {
+      const long long cofs = (long long)grp * prm.sgstride + (c0 + b);
+      const unsigned msk = (1u << prm.sin_shift) - 1u, ss = (unsigned)prm.sin_stride;
+#pragma unroll
+      for (int u = 0; u < E / SH::RL; ++u)
+#pragma unroll
+        for (int m = 0; m < SH::RL; ++m) {
+          const unsigned r = (unsigned)SH::out_elem(tt, u, m);
+          cx<T>* a = reinterpret_cast<cx<T>*>(prm.tab[r >> prm.sin_shift]) + cofs + (r & msk) * ss;
+          *a = v[u * SH::RL + m];
+        }
+    } else if (c0 + b < prm.cols) {
       cx<T>* col = reinterpret_cast<cx<T>*>(prm.data) + (long long)grp * prm.gstride + (c0 + b);
       const unsigned rs = (unsigned)prm.rstride;
 #pragma unroll
@@ -201,7 +242,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
 __host__ __device__ constexpr bool col_tma_supported(int L) { return L == 9 || L == 10; }
 
 template <typename T>
-cudaError_t launch_col_tma(int L, bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+cudaError_t launch_col_tma(int L, bool inv, bool wide, bool two, const CUtensorMap& map, const CUtensorMap& map_odd,
                            const TmaColParams& p, cudaStream_t s);
 // columns per tile (the box width) of the TMA column kernel
 template <typename T>

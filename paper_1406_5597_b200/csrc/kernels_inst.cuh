@@ -267,13 +267,13 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
   }
 }
 
-template <typename T, int L, bool INV, bool WIDE>
+template <typename T, int L, bool INV, bool WIDE, bool TWO>
 static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, const TmaColParams& p, cudaStream_t s) {
   using TC = TmaColCfg<T, L, WIDE>;
   if constexpr (!TC::OK) {
     return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
   } else {
-  auto k = col_tma_kernel<T, L, INV, WIDE>;
+  auto k = col_tma_kernel<T, L, INV, WIDE, TWO>;
   static KernelCache kc;
   const cudaError_t prep = prep_smem(k, kc, TC::SMEM);
   if (prep != cudaSuccess) return prep;
@@ -285,19 +285,27 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
   }
 }
 
+template <typename T, int L, bool TWO>
+static cudaError_t tc_dispatch2(bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+                                const TmaColParams& p, cudaStream_t s) {
+  if (wide)
+    return inv ? tc_one<T, L, true, true, TWO>(map, map_odd, p, s) : tc_one<T, L, false, true, TWO>(map, map_odd, p, s);
+  return inv ? tc_one<T, L, true, false, TWO>(map, map_odd, p, s) : tc_one<T, L, false, false, TWO>(map, map_odd, p, s);
+}
+
 template <typename T, int L>
-static cudaError_t tc_dispatch(bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
+static cudaError_t tc_dispatch(bool inv, bool wide, bool two, const CUtensorMap& map, const CUtensorMap& map_odd,
                                const TmaColParams& p, cudaStream_t s) {
-  if (wide) return inv ? tc_one<T, L, true, true>(map, map_odd, p, s) : tc_one<T, L, false, true>(map, map_odd, p, s);
-  return inv ? tc_one<T, L, true, false>(map, map_odd, p, s) : tc_one<T, L, false, false>(map, map_odd, p, s);
+  return two ? tc_dispatch2<T, L, true>(inv, wide, map, map_odd, p, s)
+             : tc_dispatch2<T, L, false>(inv, wide, map, map_odd, p, s);
 }
 
 template <>
-cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
-                                       const TmaColParams& p, cudaStream_t s) {
+cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, bool two, const CUtensorMap& map,
+                                       const CUtensorMap& map_odd, const TmaColParams& p, cudaStream_t s) {
   switch (L) {
-    case 9: return tc_dispatch<TFFFT_REAL, 9>(inv, wide, map, map_odd, p, s);
-    case 10: return tc_dispatch<TFFFT_REAL, 10>(inv, wide, map, map_odd, p, s);
+    case 9: return tc_dispatch<TFFFT_REAL, 9>(inv, wide, two, map, map_odd, p, s);
+    case 10: return tc_dispatch<TFFFT_REAL, 10>(inv, wide, two, map, map_odd, p, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -146,7 +146,15 @@ struct LocalFabric {
   std::deque<Slot> slots;
   std::atomic<int> refs{0};
 
+  // every rank's exchange events: owned by the fabric, destroyed with it, so a
+  // rank that destroys its plan early never frees an event a slower peer is
+  // still about to wait on
+  std::vector<cudaEvent_t> events;
+
   explicit LocalFabric(int p_, int dev) : p(p_), device(dev) {}
+  ~LocalFabric() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
 
   // generation barrier with abort and timeout (transport.py:225-233, 290-302)
   int barrier() {
@@ -177,6 +185,8 @@ struct LocalFabric {
   // publish this rank's buffers / events of one set (under the lock)
   void publish(int seq, int rank, int set, void* stg, void* lnd, cudaEvent_t rdy, cudaEvent_t dn) {
     std::lock_guard<std::mutex> lk(mu);
+    events.push_back(rdy);
+    events.push_back(dn);
     if ((int)slots.size() <= seq) slots.resize(seq + 1);
     Slot& s = slots[seq];
     if ((int)s.staging[set].size() != p) {
@@ -247,6 +257,7 @@ struct BufSet {
   void* staging = nullptr;    // outgoing bands, staging[q] for rank q (pull / send-recv transports)
   void* landing = nullptr;    // incoming bands, landing[s] from rank s; landing[rank] = the self band
   void** band_dst = nullptr;  // device: destination block of each outgoing band (p pointers)
+  std::vector<void*> band_dst_h;  // host copy (the TMA column kernel's store table)
   void** pull_ptrs = nullptr; // fabric pull: device list of (src, dst) per peer
   // fabric transports (local, IPC): every rank's buffers and events of this set
   std::vector<void*> peer_staging, peer_landing;
@@ -458,6 +469,17 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
+struct TwoLevelJob {
+  const void* ld_base;
+  long long cols, ngrp;
+  long long ld_in_rows, ld_blocks, ld_in, ld_out, ld_g;
+  void* st_base;
+  std::vector<void*> st_tab;
+  long long st_rows, st_in, st_g;
+};
+static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, const void* tw, cudaStream_t s,
+                           bool* done);
+
 // stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of `nplanes`
 // planes starting at `spec` (a batched p = 1 plan passes all batch * n0p planes)
 static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int nplanes) {
@@ -498,6 +520,25 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
     bool done = false;
     TRY(columns_tma(pl, pl->L1, inv, true, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
                     pl->tw1, s, &done));
+    if (done) return TFFFT_OK;
+  } else if (rd != 0) {
+    // p > 1 through the TMA column kernel: forward = plane loads + band
+    // write-redirect; inverse = landing[q][i][j][k] loads + in-place stores
+    const BufSet& B = pl->bs[pl->cur];
+    const long long n1p = pl->n1p, n2c = pl->n2c, band = (long long)pl->n0p * n1p * n2c;
+    TwoLevelJob j{};
+    j.cols = n2c;
+    j.ngrp = nplanes;
+    if (!inv) {
+      j.ld_base = spec; j.ld_in_rows = pl->n1; j.ld_blocks = 1; j.ld_in = n2c; j.ld_g = (long long)pl->n1 * n2c;
+      j.st_tab = B.band_dst_h; j.st_rows = n1p; j.st_in = n2c; j.st_g = n1p * n2c;
+    } else {
+      j.ld_base = B.landing; j.ld_in_rows = n1p; j.ld_blocks = pl->p; j.ld_in = n2c; j.ld_out = band;
+      j.ld_g = n1p * n2c;
+      j.st_base = spec; j.st_rows = pl->n1; j.st_in = n2c; j.st_g = (long long)pl->n1 * n2c;
+    }
+    bool done = false;
+    TRY(columns_tma_two(pl, pl->L1, inv, j, pl->tw1, s, &done));
     if (done) return TFFFT_OK;
   }
   CUDA_TRY(col_launch(pl, pl->L1, inv, false, rd, false, c, s));
@@ -601,8 +642,76 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
     w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
   }
   pl->launches++;
-  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, map, map_odd, w, s)
-                                               : launch_col_tma<float>(L, inv, wide, map, map_odd, w, s);
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, false, map, map_odd, w, s)
+                                               : launch_col_tma<float>(L, inv, wide, false, map, map_odd, w, s);
+  CUDA_TRY(e);
+  *done = true;
+  return TFFFT_OK;
+}
+
+// Two-level column pass at p > 1 through the TMA column kernel (col_tma.cuh,
+// TWO / 4D load mode).  Loads: a 3D map (2*cols, n, groups) with rows
+// `ld_in` apart and groups `ld_g` apart (ld_blocks == 1), or a 4D map (2*cols,
+// ld_in_rows, ld_blocks, groups) with rows `ld_in` apart, blocks `ld_out`
+// apart and groups `ld_g` apart.  Stores: uniform (st_tab empty: element r of
+// column c of group g at st_base + g * st_g + c + r * st_in) or through the
+// block table st_tab (element r at st_tab[r >> log2(st_rows)] + g * st_g + c +
+// (r mod st_rows) * st_in).  All in complex elements.  *done = false when the
+// shape or the alignment has no TMA path.
+
+
+static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, const void* tw, cudaStream_t s,
+                           bool* done) {
+  *done = false;
+  const long long esz = (long long)pl->esz, n = 1LL << L;
+  const bool two = !j.st_tab.empty();
+  if (!tma_cols_enabled(pl, L) || !col_tma_supported(L) || (int)j.st_tab.size() > kTmaTab) return TFFFT_OK;
+  if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
+      reinterpret_cast<uintptr_t>(j.ld_base) % 16)
+    return TFFFT_OK;
+  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, true) : col_tma_width<float>(L, true);
+  if (B <= 0 || j.ld_in_rows * j.ld_blocks != n) return TFFFT_OK;
+  const long long brows = std::min<long long>(std::min<long long>(n, 256), j.ld_in_rows);
+  CUtensorMap map;
+  if (j.ld_blocks == 1) {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)n, (cuuint64_t)j.ngrp};
+    cuuint64_t st[2] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n, 256), 1};
+    TRY(make_map(pl, &map, const_cast<void*>(j.ld_base), 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+  } else {
+    cuuint64_t d[4] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)j.ld_in_rows, (cuuint64_t)j.ld_blocks,
+                       (cuuint64_t)j.ngrp};
+    cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
+                        (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * B), (cuuint32_t)brows, 1, 1};
+    TRY(make_map(pl, &map, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+  }
+  TmaColParams w{};
+  w.data = j.st_base;
+  w.tw = tw;
+  w.tpg = (int)((j.cols + B - 1) / B);
+  w.ntiles = (long long)w.tpg * j.ngrp;
+  w.cols = (int)j.cols;
+  w.rstride = j.st_in;
+  w.gstride = j.st_g;
+  w.parity = 0;
+  w.load4 = j.ld_blocks > 1;
+  w.lin_shift = ilog2(j.ld_in_rows);
+  w.brows = (int)brows;
+  if (two) {
+    w.sin_shift = ilog2(j.st_rows);
+    w.sin_stride = j.st_in;
+    w.sgstride = j.st_g;
+    for (size_t q = 0; q < j.st_tab.size(); ++q) w.tab[q] = j.st_tab[q];
+  }
+  if (TFFFT_COL_TICKET && L >= ticket_min_log(true)) {
+    w.ticket = pl->col_ticket;
+    CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
+  }
+  w.evict_first = (j.ld_in * esz) % 128 == 0;
+  pl->launches++;
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, true, two, map, map, w, s)
+                                               : launch_col_tma<float>(L, inv, true, two, map, map, w, s);
   CUDA_TRY(e);
   *done = true;
   return TFFFT_OK;
@@ -715,6 +824,29 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
                          ((long long)pl->n1 * pl->n2c * (long long)pl->esz) % pfb == 0;
     c.pf_ahead = aligned ? ahead : 0;
     c.pf_bytes = pfb;
+  }
+  if (pl->p > 1) {
+    // p > 1 through the TMA column kernel: forward = landing[s][i][c] loads +
+    // in-place two-level stores; inverse = two-level loads + block redirect
+    const BufSet& B = pl->bs[pl->cur];
+    const long long n1p = pl->n1p, n2c = pl->n2c, band = (long long)pl->n0p * n1p * n2c;
+    TwoLevelJob j{};
+    j.cols = n1p * n2c;
+    j.ngrp = 1;
+    j.ld_in_rows = pl->n0p;
+    j.ld_blocks = pl->p;
+    j.st_rows = pl->n0p;
+    if (!inv) {
+      j.ld_base = B.landing; j.ld_in = n1p * n2c; j.ld_out = band;
+      for (int q = 0; q < pl->p; ++q) j.st_tab.push_back(static_cast<char*>(spec) + (size_t)q * n1p * n2c * pl->esz);
+      j.st_in = (long long)pl->n1 * n2c;
+    } else {
+      j.ld_base = spec; j.ld_in = (long long)pl->n1 * n2c; j.ld_out = n1p * n2c;
+      j.st_tab = B.band_dst_h; j.st_in = n1p * n2c;
+    }
+    bool done = false;
+    TRY(columns_tma_two(pl, pl->L0, inv, j, pl->tw0, s, &done));
+    if (done) return TFFFT_OK;
   }
   int rd = 0;
   if (pl->p > 1) {
@@ -845,6 +977,7 @@ static int build_band_dst(tffft_plan_t pl, int set) {
   }
   if (!B.band_dst) CUDA_TRY(cudaMalloc(&B.band_dst, sizeof(void*) * pl->p));
   CUDA_TRY(cudaMemcpy(B.band_dst, h.data(), sizeof(void*) * pl->p, cudaMemcpyHostToDevice));
+  B.band_dst_h = h;
   return TFFFT_OK;
 }
 
@@ -969,7 +1102,6 @@ static int fabric_setup_local(tffft_plan_t pl) {
     cudaEvent_t rdy, dn;
     CUDA_TRY(cudaEventCreateWithFlags(&rdy, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&dn, cudaEventDisableTiming));
-    B.own_events = true;
     fab.publish(pl->seq, pl->rank, st, B.staging, B.landing, rdy, dn);
   }
   TRY(fab.barrier());
@@ -1188,6 +1320,14 @@ int tffft_comm_init_local(int p, int device, tffft_comm_t* comms) {
     comms[r] = c;
   }
   return TFFFT_OK;
+}
+
+// host barrier of a local-fabric or IPC communicator (Endpoint.barrier's
+// rank-meeting half, cli.py:102, 106); NCCL communicators have no host barrier
+int tffft_comm_barrier(tffft_comm_t c) {
+  if (!c) return fail(TFFFT_ERR_CONFIGURATION, "null communicator");
+  if (c->kind == COMM_NCCL) return fail(TFFFT_ERR_CONFIGURATION, "NCCL communicators have no host barrier");
+  return c->barrier();
 }
 
 int tffft_comm_check(tffft_comm_t c) {
@@ -1415,7 +1555,7 @@ int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, in
   pl->esz = dtype == TFFFT_F64 ? 16 : 8;
   pl->batch = batch;
   pl->strategy = strategy;
-  pl->tma_cols = (p == 1 && strategy == 0) ? tma_cols : 0;
+  pl->tma_cols = strategy == 0 ? tma_cols : 0;
   CUDA_TRY(cudaSetDevice(comm->device));
 
   size_t ws = 0;

@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import torch
 
-from .dfft import FftPlan, forward, inverse
+from .dfft import FftPlan, forward, forward_many, inverse, inverse_many
 from .layout import RealSlab
 
 __all__ = ["HostPairStream"]
@@ -31,7 +31,8 @@ class HostPairStream:
 
     def run(self, host_in: list[torch.Tensor], host_out: list[torch.Tensor]) -> None:
         """Transform host_in[i] -> host_out[i] (pinned host tensors of the real
-        slab size) for every i; returns when all results are on the host."""
+        slab size, times fp.batch for a batched plan) for every i; returns when
+        all results are on the host."""
         fp, dev = self.fp, self.fp.device
         n, depth = len(host_in), self.depth
         in_ready = [torch.cuda.Event() for _ in range(n)]
@@ -55,9 +56,14 @@ class HostPairStream:
                 self.compute.wait_event(in_ready[i])
                 if i >= depth:
                     self.compute.wait_event(out_free[i - depth])  # download(i - depth) done
-                spec = forward(fp, RealSlab(fp.real_layout, self.d_in[b]))
-                in_free[i].record(self.compute)
-                inverse(fp, spec, out=self.d_out[b])
+                if fp.batch > 1:  # a batched plan: every step carries fp.batch fields
+                    spec = forward_many(fp, self.d_in[b])
+                    in_free[i].record(self.compute)
+                    inverse_many(fp, spec, out=self.d_out[b])
+                else:
+                    spec = forward(fp, RealSlab(fp.real_layout, self.d_in[b]))
+                    in_free[i].record(self.compute)
+                    inverse(fp, spec, out=self.d_out[b])
                 out_ready[i].record(self.compute)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(out_ready[i])
