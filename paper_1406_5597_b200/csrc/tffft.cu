@@ -1785,17 +1785,52 @@ static int check_ready(tffft_plan_t pl) {
 }
 
 // stage 1 (dfft.py:161-163) of `nf` fields at (real, spec): r2c rows + n1 columns
+// planes per chunk of the plane-interleaved stage 1 (TFFFT_S1_CHUNK, 0 = off):
+// the n1 columns of a chunk run right after its rows, while the chunk is
+// still L2-resident, so the column pass reads and overwrites it in L2
+static int s1_chunk(tffft_plan_t pl) {
+  static const int v = [] {
+    const char* e = getenv("TFFFT_S1_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  return (v > 0 && pl->p == 1) ? v : 0;
+}
+
 static int fwd_stage1(tffft_plan_t pl, const void* real, void* spec, int nf, cudaStream_t s) {
   NvtxRange r("stage1");
   if (pl->s1_fused) return stage1_fused(pl, const_cast<void*>(real), spec, true, s);
-  CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real), spec, nf * pl->n0p, 0), s));
-  return stage1_columns(pl, spec, false, s, nf * pl->n0p);
+  const int planes = nf * pl->n0p, K = s1_chunk(pl);
+  if (K > 0 && K < planes) {
+    const size_t rb = (size_t)pl->n1 * pl->n2 * (pl->esz / 2), sb = (size_t)pl->n1 * pl->n2c * pl->esz;
+    for (int a = 0; a < planes; a += K) {
+      const int k = std::min(K, planes - a);
+      const char* rr = static_cast<const char*>(real) + (size_t)a * rb;
+      char* ss = static_cast<char*>(spec) + (size_t)a * sb;
+      CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<char*>(rr), ss, k, a), s));
+      TRY(stage1_columns(pl, ss, false, s, k));
+    }
+    return TFFFT_OK;
+  }
+  CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<void*>(real), spec, planes, 0), s));
+  return stage1_columns(pl, spec, false, s, planes);
 }
 // stage 1' (dfft.py:206-209) of one field (component c of the batch) or, at
 // p = 1, of `nf` fields: n1 columns + c2r rows with 1/(n0 n1 n2)
 static int inv_stage1(tffft_plan_t pl, void* spec, void* real, int nf, int c, cudaStream_t s) {
   NvtxRange r("stage1");
   if (pl->s1_fused) return stage1_fused(pl, real, spec, false, s);
+  const int planes = nf * pl->n0p, K = s1_chunk(pl);
+  if (K > 0 && K < planes) {
+    const size_t rb = (size_t)pl->n1 * pl->n2 * (pl->esz / 2), sb = (size_t)pl->n1 * pl->n2c * pl->esz;
+    for (int a = 0; a < planes; a += K) {
+      const int k = std::min(K, planes - a);
+      char* ss = static_cast<char*>(spec) + (size_t)a * sb;
+      TRY(stage1_columns(pl, ss, true, s, k));
+      CUDA_TRY(c2r_launch(pl, row_params(pl, static_cast<char*>(real) + (size_t)a * rb, ss, k,
+                                         (long long)c * pl->n0p + a), s));
+    }
+    return TFFFT_OK;
+  }
   TRY(stage1_columns(pl, spec, true, s, nf * pl->n0p));
   TRY(landing_consumed(pl, s));
   CUDA_TRY(c2r_launch(pl, row_params(pl, real, spec, nf * pl->n0p, (long long)c * pl->n0p), s));

@@ -381,18 +381,21 @@ def test_collective_pattern_matches_pairwise(shape, p, strategy):
         assert rel(b[1], x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL["float64"]
 
 
-TMA_CASES = [((512, 8, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((512, 512, 8), 1), ((64, 512, 32), 2)]
+TMA_CASES = [((512, 8, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((512, 512, 8), 1), ((64, 512, 32), 2),
+             ((1024, 64, 16), 2), ((512, 512, 8), 4), ((1024, 32, 64), 8), ((32, 1024, 16), 4),
+             ((1024, 16, 8), 16)]
 
 
 @pytest.mark.parametrize("shape,p", TMA_CASES, ids=lambda v: str(v))
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_tma_column_kernel_bitwise(shape, p, dtype):
-    """TMA-fed column passes (col_tma.cuh, lengths 512 / 1024, p = 1): the same
+    """TMA-fed column passes (col_tma.cuh, lengths 512 / 1024): the same
     Stockham arithmetic as the cp.async kernel, so spectra and inverse outputs
-    are bitwise identical to the default kernels, and within tolerance of the
+    are bitwise identical to the cp.async kernels, and within tolerance of the
     oracle.  Covers partial tiles (columns not a multiple of the box width),
-    float32 stage 1b (row stride not 16-byte aligned: falls back) and p = 2
-    (the flag is dropped: the TMA path is single-rank)."""
+    float32 stage 1b (row stride not 16-byte aligned: falls back), and p > 1:
+    the two-level variant (4D landing loads, block-table stores) at
+    p = 2 .. 16, including blocks shorter than a 256-row box."""
     x = oracle.uniform_field(shape, seed=31)
     if dtype == "float32":
         x = x.astype(np.float32).astype(np.float64)
@@ -402,7 +405,7 @@ def test_tma_column_kernel_bitwise(shape, p, dtype):
     def body(ep):
         ref = tf.plan(grid, ep, dtype=dtype, algorithms=())
         fp = tf.plan(grid, ep, dtype=dtype, algorithms=("tma_columns",))
-        assert fp.algorithms == (("tma_columns",) if p == 1 else ())
+        assert fp.algorithms == ("tma_columns",)
         want = tf.forward(ref, slabs[ep.rank]).data.clone()
         want_back = tf.inverse(ref, tf.SpectralSlab(ref.spectral_layout, tf.SpectralTag.STRIDED_INPLACE,
                                                       want.clone())).data.clone()
