@@ -54,19 +54,31 @@ namespace tffft {
 __device__ __forceinline__ void st_cs(cx<double>* a, cx<double> z) { __stcs(reinterpret_cast<double2*>(a), make_double2(z.x, z.y)); }
 __device__ __forceinline__ void st_cs(cx<float>* a, cx<float> z) { __stcs(reinterpret_cast<float2*>(a), make_float2(z.x, z.y)); }
 
-template <typename T, int L, bool WIDE>
+// FPF (full prefetch): the whole next tile streams into a dedicated region as
+// soon as the current tile's operands are read, and the Stockham exchange runs
+// in a separate, half-size buffer of real words (re round, then im round).
+// Without FPF the next tile's second half must wait for the exchange buffer
+// to drain (about half a tile later).
+template <typename T, int L, bool WIDE, bool FPF = false>
 struct TmaColCfg {
   using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
   static constexpr int N = SH::N, B = CF::B, THREADS = CF::THREADS;
   static constexpr int BOX = N < 256 ? N : 256;   // rows per TMA box (hardware limit 256)
   static constexpr int NBOX = N / BOX;
-  static constexpr int NPF = NBOX > 1 ? NBOX / 2 : 1;  // boxes landing in the prefetch region
+  static constexpr int NPF = NBOX > 1 ? NBOX / 2 : 1;  // boxes of the first half
   static constexpr size_t BOXB = sizeof(cx<T>) * (size_t)BOX * B;
-  static constexpr size_t PF = BOXB * NPF;
   // the odd-row boxes of the parity mode are two complex wider (pitch B + 2)
   static constexpr size_t XB = sizeof(cx<T>) * (size_t)BOX * (B + 2) * (NBOX - NPF);
-  static constexpr size_t X = CF::X_BYTES > XB ? CF::X_BYTES : XB;
+  // FPF exchange buffer: real words, column stride SS (one pad word per E
+  // words; B columns x QW / B threads per wavefront cover every bank once)
+  static constexpr int QWS = 128 / (int)sizeof(T);
+  static constexpr int SS = ((CF::RAW + QWS - 1) / QWS) * QWS + (QWS / B > 0 ? QWS / B : 1);
+  static constexpr size_t XS = sizeof(T) * (size_t)B * SS;
+  static constexpr size_t PF = FPF ? BOXB * NPF + XB : BOXB * NPF;  // FPF: both halves (odd rows wider)
+  static constexpr size_t X = FPF ? XS : (CF::X_BYTES > XB ? CF::X_BYTES : XB);
+  static constexpr int S = FPF ? SS : CF::S;
+  static constexpr bool SPLIT = FPF ? true : CF::SPLIT;
   static constexpr int TW = SH::TW > 0 ? SH::TW : 1;
   static constexpr size_t SMEM = PF + X + sizeof(cx<T>) * TW + 64;
   static constexpr bool OK = CF::CL == 1 && CF::GROUPS == 1 && CF::XCHG && SMEM <= 227 * 1024 &&
@@ -97,22 +109,23 @@ struct TmaColParams {
   void* tab[kTmaTab];    // TWO stores: block base pointers
 };
 
-template <typename T, int L, bool INV, bool WIDE, bool TWO>
+template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
 __global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, 1)
 col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_odd,
                const TmaColParams prm) {
-  using TC = TmaColCfg<T, L, WIDE>;
+  using TC = TmaColCfg<T, L, WIDE, FPF>;
   using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
-  using ST = Stockham<T, L, INV, CF::S, CF::PS, CF::SPLIT, 0, true>;
+  using ST = Stockham<T, L, INV, TC::S, CF::PS, TC::SPLIT, 0, true>;
   constexpr int E = SH::E, TPT = SH::TPT, B = TC::B, BOX = TC::BOX;
   static_assert(TC::OK, "unsupported column-kernel shape for the TMA path");
   static_assert(BOX % TPT == 0, "a thread's operand rows tt + TPT kk stay inside box (TPT kk) / BOX");
 
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   cx<T>* pf = reinterpret_cast<cx<T>*>(smem_tc);                       // boxes [0, NPF)
-  unsigned char* xs = smem_tc + TC::PF;                                // exchange buffer / boxes [NPF, NBOX)
-  cx<T>* xb = reinterpret_cast<cx<T>*>(xs);
+  unsigned char* xs = smem_tc + TC::PF;                                // exchange buffer
+  // boxes [NPF, NBOX): behind the first half (FPF) or in the exchange buffer
+  cx<T>* xb = FPF ? pf + (size_t)TC::BOX * B * TC::NPF : reinterpret_cast<cx<T>*>(xs);
   cx<T>* s_tw = reinterpret_cast<cx<T>*>(xs + TC::X);
   uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(s_tw) + sizeof(cx<T>) * TC::TW);
 
@@ -197,11 +210,14 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     __syncthreads();  // every operand read: both halves may be overwritten
     if (t == 0) {
       if (dyn) s_tk[(i + 1) & 1] = (long long)atomicAdd(prm.ticket, 1ull);  // read next iteration, after the exchange barriers
-      if (nxt < prm.ntiles) load_half(nxt, 0);
+      if (nxt < prm.ntiles) {
+        load_half(nxt, 0);
+        if (FPF) load_half(nxt, 1);
+      }
     }
     ST::first(v, tt, s_tw);
     auto hook = [&] {  // the last exchange has drained the buffer
-      if (t == 0 && nxt < prm.ntiles) load_half(nxt, 1);
+      if (!FPF && t == 0 && nxt < prm.ntiles) load_half(nxt, 1);
     };
     ST::finish(xs, v, tt, b, s_tw, hook);
     int grp, c0;
@@ -244,6 +260,7 @@ __host__ __device__ constexpr bool col_tma_supported(int L) { return L == 9 || L
 template <typename T>
 cudaError_t launch_col_tma(int L, bool inv, bool wide, bool two, const CUtensorMap& map, const CUtensorMap& map_odd,
                            const TmaColParams& p, cudaStream_t s);
+// the full-prefetch variant is the default for WIDE passes (TFFFT_TMA_FPF=0 disables it, launch_col_tma)
 // columns per tile (the box width) of the TMA column kernel
 template <typename T>
 int col_tma_width(int L, bool wide);

@@ -267,13 +267,13 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
   }
 }
 
-template <typename T, int L, bool INV, bool WIDE, bool TWO>
+template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
 static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, const TmaColParams& p, cudaStream_t s) {
-  using TC = TmaColCfg<T, L, WIDE>;
+  using TC = TmaColCfg<T, L, WIDE, FPF>;
   if constexpr (!TC::OK) {
     return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
   } else {
-  auto k = col_tma_kernel<T, L, INV, WIDE, TWO>;
+  auto k = col_tma_kernel<T, L, INV, WIDE, TWO, FPF>;
   static KernelCache kc;
   const cudaError_t prep = prep_smem(k, kc, TC::SMEM);
   if (prep != cudaSuccess) return prep;
@@ -285,12 +285,31 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
   }
 }
 
+// full-prefetch variant (col_tma.cuh FPF), the default for the WIDE (128-byte
+// row) column passes; TFFFT_TMA_FPF=0 selects the half-and-half prefetch.
+// Measured at 1024^3 (profiles/r02/fpf_ab.txt): isolated (ncu) 3.00 vs 2.97 ms
+// per launch, but in the live pair at the power cap stage 3 + 3' take
+// 6.61-6.76 ms instead of 7.00-7.05 (float32: 3.31 vs 3.43 ms).
+static bool tma_fpf() {
+  static const bool v = [] {
+    const char* e = getenv("TFFFT_TMA_FPF");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 template <typename T, int L, bool TWO>
 static cudaError_t tc_dispatch2(bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
                                 const TmaColParams& p, cudaStream_t s) {
-  if (wide)
-    return inv ? tc_one<T, L, true, true, TWO>(map, map_odd, p, s) : tc_one<T, L, false, true, TWO>(map, map_odd, p, s);
-  return inv ? tc_one<T, L, true, false, TWO>(map, map_odd, p, s) : tc_one<T, L, false, false, TWO>(map, map_odd, p, s);
+  if (wide) {
+    if (tma_fpf() && TmaColCfg<T, L, true, true>::OK)
+      return inv ? tc_one<T, L, true, true, TWO, true>(map, map_odd, p, s)
+                 : tc_one<T, L, false, true, TWO, true>(map, map_odd, p, s);
+    return inv ? tc_one<T, L, true, true, TWO, false>(map, map_odd, p, s)
+               : tc_one<T, L, false, true, TWO, false>(map, map_odd, p, s);
+  }
+  return inv ? tc_one<T, L, true, false, TWO, false>(map, map_odd, p, s)
+             : tc_one<T, L, false, false, TWO, false>(map, map_odd, p, s);
 }
 
 template <typename T, int L>
@@ -317,6 +336,7 @@ int col_tma_width<TFFFT_REAL>(int L, bool wide) {
                         : (TmaColCfg<TFFFT_REAL, 9, false>::OK ? TmaColCfg<TFFFT_REAL, 9, false>::B : 0);
     case 10: return wide ? (TmaColCfg<TFFFT_REAL, 10, true>::OK ? TmaColCfg<TFFFT_REAL, 10, true>::B : 0)
                          : (TmaColCfg<TFFFT_REAL, 10, false>::OK ? TmaColCfg<TFFFT_REAL, 10, false>::B : 0);
+    // (the full-prefetch variant has the same box width)
     default: return 0;
   }
 }
