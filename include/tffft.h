@@ -176,6 +176,10 @@ int tffft_reset_instrumentation(tffft_plan_t plan);
  * largest discarded imaginary magnitude and TFFFT_ERR_CONSISTENCY when a plane
  * violates the reference tolerance 1e-9*n2*max|X| (kernels.py:223-238). */
 int tffft_consistency(tffft_plan_t plan, double* residue);
+/* debug: fill the plan's exchange staging / landing buffers and c2r row
+ * records with 0xFF bytes (NaN), so a read of an element no stage wrote shows
+ * up as NaN in the output; synchronous */
+int tffft_plan_poison(tffft_plan_t plan);
 /* number of kernels this library launched on the plan since the last reset */
 int tffft_launch_count(tffft_plan_t plan, uint64_t* launches);
 

@@ -208,14 +208,19 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
 #pragma unroll
     for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = operand(kk);
     __syncthreads();  // every operand read: both halves may be overwritten
+    unsigned long long tk = 0;
     if (t == 0) {
-      if (dyn) s_tk[(i + 1) & 1] = (long long)atomicAdd(prm.ticket, 1ull);  // read next iteration, after the exchange barriers
+      // the next tile's boxes first, then the ticket after next: its atomic
+      // returns while pass 0 computes (storing it right away would hold the
+      // loads behind the atomic's round trip)
       if (nxt < prm.ntiles) {
         load_half(nxt, 0);
         if (FPF) load_half(nxt, 1);
       }
+      if (dyn) tk = atomicAdd(prm.ticket, 1ull);
     }
     ST::first(v, tt, s_tw);
+    if (t == 0 && dyn) s_tk[(i + 1) & 1] = (long long)tk;  // read next iteration, after the exchange barriers
     auto hook = [&] {  // the last exchange has drained the buffer
       if (!FPF && t == 0 && nxt < prm.ntiles) load_half(nxt, 1);
     };

@@ -2016,6 +2016,29 @@ int tffft_inverse(tffft_plan_t pl, void* spec_inout, void* real_out, void* strea
   return TFFFT_OK;
 }
 
+// Debug aid (compute-sanitizer is closed on this pool): fill every
+// plan-internal buffer that a stage reads after another stage or rank wrote
+// it -- exchange staging and landing of every set, the c2r row records -- with
+// 0xFF bytes (a NaN in either precision).  A kernel that reads an element
+// nobody wrote, or reads it before it was written, then turns the output into
+// NaN (tests/test_gpu_races.py).  Synchronous.
+int tffft_plan_poison(tffft_plan_t pl) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const size_t band = band_bytes(pl);
+  for (int st = 0; st < 2; ++st) {
+    BufSet& B = pl->bs[st];
+    const size_t sb = pl->p > 1 ? (size_t)pl->p * band : band;
+    if (B.staging) CUDA_TRY(cudaMemset(B.staging, 0xFF, sb));
+    if (B.landing) CUDA_TRY(cudaMemset(B.landing, 0xFF, sb));
+  }
+  if (!pl->s1_fused)
+    CUDA_TRY(cudaMemset(pl->row_stats, 0xFF, sizeof(double) * 3 * (size_t)pl->batch * pl->n0p * pl->n1));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return TFFFT_OK;
+}
+
 int tffft_plan_batch(tffft_plan_t pl, int* batch) {
   if (!pl || !batch) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   *batch = pl->batch;

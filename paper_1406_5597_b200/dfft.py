@@ -104,6 +104,12 @@ class FftPlan:
         _lib.check(_lib.lib().tffft_plan_workspace_bytes(self.handle, ctypes.byref(n)))
         return int(n.value)
 
+    def poison(self) -> None:
+        """Debug: fill the plan's exchange buffers and row records with NaN
+        (tffft_plan_poison); a stage reading an element no stage wrote then
+        yields NaN.  Synchronous."""
+        _lib.check(_lib.lib().tffft_plan_poison(self.handle))
+
     def close(self) -> None:
         if self.handle:
             _lib.lib().tffft_plan_destroy(self.handle)
