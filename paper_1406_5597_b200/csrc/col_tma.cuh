@@ -107,6 +107,8 @@ struct TmaColParams {
   long long sin_stride;  // TWO stores: elements between the rows of a block
   long long sgstride;    // TWO stores: elements between groups
   void* tab[kTmaTab];    // TWO stores: block base pointers
+  int tma_store;         // FPF, in place through `map` (parity 0): the first half of each output tile leaves
+                         // through TMA boxes staged in the drained exchange buffer, the rest through STG
 };
 
 template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
@@ -117,7 +119,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
   using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
   using ST = Stockham<T, L, INV, TC::S, CF::PS, TC::SPLIT, 0, true>;
-  constexpr int E = SH::E, TPT = SH::TPT, B = TC::B, BOX = TC::BOX;
+  constexpr int E = SH::E, TPT = SH::TPT, B = TC::B, BOX = TC::BOX, N = SH::N;
   static_assert(TC::OK, "unsupported column-kernel shape for the TMA path");
   static_assert(BOX % TPT == 0, "a thread's operand rows tt + TPT kk stay inside box (TPT kk) / BOX");
 
@@ -207,6 +209,8 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     cx<T> v[E];
 #pragma unroll
     for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = operand(kk);
+    // the previous tile's TMA store has read its staging (the exchange buffer)
+    if (FPF && !TWO && t == 0 && prm.tma_store) bulk_wait_read0();
     __syncthreads();  // every operand read: both halves may be overwritten
     unsigned long long tk = 0;
     if (t == 0) {
@@ -227,6 +231,36 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     ST::finish(xs, v, tt, b, s_tw, hook);
     int grp, c0;
     coords(cur, grp, c0);
+    if constexpr (FPF && !TWO) {
+      if (prm.tma_store) {
+        // rows [0, N/2): stage them as the [row][B] box layout in the drained
+        // exchange buffer and store them with N/2/BOX TMA boxes; the other half
+        // leaves from registers below
+        cx<T>* ob = reinterpret_cast<cx<T>*>(xs);
+#pragma unroll
+        for (int u = 0; u < E / SH::RL; ++u)
+#pragma unroll
+          for (int m = 0; m < SH::RL; ++m)
+            if ((TPT * u + m * (N / SH::RL)) < N / 2) ob[SH::out_elem(tt, u, m) * B + b] = v[u * SH::RL + m];
+        fence_async_shared();
+        __syncthreads();
+        if (t == 0) {
+          for (int q = 0; q < TC::NPF; ++q) tma_store3(&map, 2 * c0, q * BOX, grp, ob + (size_t)q * BOX * B, pol);
+          bulk_commit();
+        }
+        if (c0 + b < prm.cols) {
+          cx<T>* col = reinterpret_cast<cx<T>*>(prm.data) + (long long)grp * prm.gstride + (c0 + b);
+          const unsigned rs = (unsigned)prm.rstride;
+#pragma unroll
+          for (int u = 0; u < E / SH::RL; ++u)
+#pragma unroll
+            for (int m = 0; m < SH::RL; ++m)
+              if ((TPT * u + m * (N / SH::RL)) >= N / 2) col[(unsigned)SH::out_elem(tt, u, m) * rs] = v[u * SH::RL + m];
+        }
+        cur = nxt;
+        continue;
+      }
+    }
     if (TWO && c0 + b < prm.cols) {
       const long long cofs = (long long)grp * prm.sgstride + (c0 + b);
       const unsigned msk = (1u << prm.sin_shift) - 1u, ss = (unsigned)prm.sin_stride;
@@ -257,6 +291,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     }
     cur = nxt;
   }
+  if (FPF && !TWO && t == 0 && prm.tma_store) bulk_wait0();  // the staging must outlive the last TMA store
 }
 
 // lengths with a TMA-fed column kernel

@@ -640,6 +640,9 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   {
     static const char* ef = getenv("TFFFT_TMA_EF");
     w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
+    // half of each output tile through TMA stores (in place, single map)
+    static const char* ts = getenv("TFFFT_TMA_STORE");
+    w.tma_store = (!parity && ts && atoi(ts) != 0) ? 1 : 0;
   }
   pl->launches++;
   const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, wide, false, map, map_odd, w, s)
