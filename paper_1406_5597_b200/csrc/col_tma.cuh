@@ -68,8 +68,9 @@ struct TmaColCfg {
   static constexpr int NBOX = N / BOX;
   static constexpr int NPF = NBOX > 1 ? NBOX / 2 : 1;  // boxes of the first half
   static constexpr size_t BOXB = sizeof(cx<T>) * (size_t)BOX * B;
-  // the odd-row boxes of the parity mode are two complex wider (pitch B + 2)
-  static constexpr size_t XB = sizeof(cx<T>) * (size_t)BOX * (B + 2) * (NBOX - NPF);
+  // the odd-row boxes of the parity mode (float32 rows only) are two complex
+  // wider (pitch B + 2)
+  static constexpr size_t XB = sizeof(cx<T>) * (size_t)BOX * (sizeof(T) == 4 ? B + 2 : B) * (NBOX - NPF);
   // FPF exchange buffer: real words, column stride SS (one pad word per E
   // words; B columns x QW / B threads per wavefront cover every bank once)
   static constexpr int QWS = 128 / (int)sizeof(T);
@@ -111,8 +112,12 @@ struct TmaColParams {
                          // through TMA boxes staged in the drained exchange buffer, the rest through STG
 };
 
+// resident CTAs per SM the TMA column kernel is compiled for (register cap)
+#ifndef TFFFT_TMA_MINB
+#define TFFFT_TMA_MINB 1
+#endif
 template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
-__global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, 1)
+__global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, TFFFT_TMA_MINB)
 col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_odd,
                const TmaColParams prm) {
   using TC = TmaColCfg<T, L, WIDE, FPF>;
@@ -174,7 +179,8 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     const int q0 = h ? TC::NPF : 0, q1 = h ? TC::NBOX : TC::NPF;
     if (q1 <= q0) return;
     fence_async_shared();  // the CTA's generic accesses to the region are ordered before the TMA writes
-    const int pitch = (prm.parity && h) ? B + 2 : B;
+    const bool par = sizeof(T) == 4 && prm.parity;  // float64 rows are always 16-byte aligned
+    const int pitch = (par && h) ? B + 2 : B;
     mbar_arrive_tx(bar + h, (unsigned)(sizeof(cx<T>) * (size_t)BOX * pitch * (q1 - q0)));
     cx<T>* dst = h ? xb : pf;
     if (prm.load4) {  // two-level rows: boxes of brows rows, never across a block
@@ -184,7 +190,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
       return;
     }
     for (int q = q0; q < q1; ++q) {
-      if (prm.parity)
+      if (par)
         tma_load3(dst + (size_t)(q - q0) * BOX * pitch, h ? &map_odd : &map, 2 * c0, (q - q0) * BOX, grp, bar + h,
                   pol);
       else
@@ -193,7 +199,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
   };
   auto operand = [&](int kk) -> cx<T> {  // row tt + TPT kk; kk is a compile-time constant after unrolling
     const int r = tt + TPT * kk;
-    if (prm.parity) return (tt & 1) ? xb[(r >> 1) * (B + 2) + 1 + b] : pf[(r >> 1) * B + b];
+    if (sizeof(T) == 4 && prm.parity) return (tt & 1) ? xb[(r >> 1) * (B + 2) + 1 + b] : pf[(r >> 1) * B + b];
     return (TPT * kk) / BOX < TC::NPF ? pf[r * B + b] : xb[(r - TC::NPF * BOX) * B + b];
   };
 

@@ -76,6 +76,10 @@ struct RowParams {
 #ifndef TFFFT_SPLIT
 #define TFFFT_SPLIT 0
 #endif
+// fewest threads of a column CTA (columns are added until reached)
+#ifndef TFFFT_COL_MINTHREADS
+#define TFFFT_COL_MINTHREADS 256
+#endif
 #ifndef TFFFT_PREFETCH
 #define TFFFT_PREFETCH 1
 #endif
@@ -108,7 +112,7 @@ template <typename T, int L, bool WIDE>
 __host__ __device__ constexpr int col_batch() {
   constexpr int TPT = Shape<L>::TPT, N = Shape<L>::N;
   constexpr int want = WIDE ? TFFFT_COLB * (int)(16 / sizeof(cx<T>)) : TFFFT_NARROW_B;
-  int b = 256 / TPT > want ? 256 / TPT : want;
+  int b = TFFFT_COL_MINTHREADS / TPT > want ? TFFFT_COL_MINTHREADS / TPT : want;
   // split exchange: prefetch slots (complex) + exchange buffer (real words);
   // whole-complex exchange: the next tile's operands fit slots + exchange buffer
   constexpr size_t per_elem = TFFFT_SPLIT ? sizeof(cx<T>) + sizeof(T) : sizeof(cx<T>);

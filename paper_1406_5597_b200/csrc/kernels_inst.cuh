@@ -278,7 +278,9 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
   const cudaError_t prep = prep_smem(k, kc, TC::SMEM);
   if (prep != cudaSuccess) return prep;
   if (p.ntiles <= 0) return cudaSuccess;
-  const long long blocks = std::min<long long>(p.ntiles, num_sms());
+  // persistent: every resident CTA slot of the GPU (one per SM at 216 registers)
+  const long long blocks =
+      std::min<long long>(p.ntiles, (long long)occupancy(k, kc, TC::THREADS, TC::SMEM) * num_sms());
   (void)cudaGetLastError();
   k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, map_odd, p);
   return cudaGetLastError();

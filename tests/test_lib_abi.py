@@ -131,3 +131,51 @@ def test_comm_check_local_fabric_is_healthy():
     finally:
         for r in range(2):
             lib.tffft_comm_destroy(arr[r])
+
+
+def test_round2_entry_points_validate_on_the_host():
+    """Host-side argument checks of the round-2 C ABI (no GPU needed):
+    comm_init_all refuses a device listed twice (NCCL needs one GPU per rank),
+    plan_create_batched refuses batch < 1, comm_init_ipc needs a barrier,
+    comm_barrier is refused on NCCL-kind communicators and passes on a p = 1
+    local fabric, ipc export is refused on local-fabric plans."""
+    lib = _lib.lib()
+    comms = (ctypes.c_void_p * 2)()
+    with pytest.raises(tf.ConfigurationError, match="listed twice"):
+        _lib.check(lib.tffft_comm_init_all(2, (ctypes.c_int * 2)(0, 0), comms))
+    one = (ctypes.c_void_p * 1)()
+    _lib.check(lib.tffft_comm_init_all(1, (ctypes.c_int * 1)(0), one))  # p = 1: no NCCL needed
+    with pytest.raises(tf.ConfigurationError):
+        _lib.check(lib.tffft_comm_barrier(one[0]))
+    lib.tffft_comm_destroy(one[0])
+    arr = (ctypes.c_void_p * 1)()
+    _lib.check(lib.tffft_comm_init_local(1, 0, arr))
+    _lib.check(lib.tffft_comm_barrier(arr[0]))
+    h = ctypes.c_void_p()
+    with pytest.raises(tf.ConfigurationError, match="batch"):
+        _lib.check(lib.tffft_plan_create_batched(8, 8, 8, 0, 0, 0, 0, arr[0], ctypes.byref(h)))
+    with pytest.raises(tf.ConfigurationError):
+        _lib.check(lib.tffft_plan_ipc_export(None, None))
+    lib.tffft_comm_destroy(arr[0])
+    ipc = ctypes.c_void_p()
+    with pytest.raises(tf.ConfigurationError):
+        _lib.check(lib.tffft_comm_init_ipc(2, 0, 0, None, None, ctypes.byref(ipc)))
+    with pytest.raises(tf.ConfigurationError):
+        _lib.check(lib.tffft_comm_init_ipc(2, 5, 0, ctypes.cast(_lib.BARRIER_FN(lambda c: 0), ctypes.c_void_p), None,
+                                           ctypes.byref(ipc)))
+
+
+def test_ipc_barrier_callback_failure_is_a_transport_error():
+    """A failing host barrier (the callback returns non-zero) surfaces as
+    TransportError, and the communicator stays aborted (transport.py:209-219)."""
+    lib = _lib.lib()
+    cb = _lib.BARRIER_FN(lambda ctx: 1)
+    c = ctypes.c_void_p()
+    _lib.check(lib.tffft_comm_init_ipc(2, 0, 0, ctypes.cast(cb, ctypes.c_void_p), None, ctypes.byref(c)))
+    try:
+        with pytest.raises(tf.TransportError):
+            _lib.check(lib.tffft_comm_barrier(c))
+        with pytest.raises(tf.TransportError, match="aborted"):
+            _lib.check(lib.tffft_comm_barrier(c))
+    finally:
+        lib.tffft_comm_destroy(c)
