@@ -59,11 +59,29 @@ __device__ __forceinline__ void st_cs(cx<float>* a, cx<float> z) { __stcs(reinte
 // in a separate, half-size buffer of real words (re round, then im round).
 // Without FPF the next tile's second half must wait for the exchange buffer
 // to drain (about half a tile later).
-template <typename T, int L, bool WIDE, bool FPF = false>
+// Columns per CTA: WIDE passes (stage 3 / 3', rows megabytes apart) take
+// 128-byte row segments -- 8 float64 or 16 float32 columns at 1024 points (at
+// least 256 threads), one CTA per SM; NARROW passes (stage 1b / 1b', rows n2c
+// elements apart) may take half as many columns, two CTAs per SM
+// (TFFFT_TMA_NARROW=1; profiles/r02/narrow_ab.txt: slower in isolation and no
+// gain live, so off; at the 8.4 MB stage-3 stride 64-byte boxes over-fetch
+// 1.5x and are much slower, profiles/r02/b4_ab.txt).
+template <typename T, int L>
+__host__ __device__ constexpr int tma_cols_per_cta(bool wide) {
+  // wide: 128-byte rows and at least 256 threads; narrow: half of that
+  const int rowc = 8 * (int)(16 / sizeof(cx<T>)), tpt = Shape<L>::TPT;
+  const int w = 256 / tpt > rowc ? 256 / tpt : rowc;
+  return wide ? w : w / 2;
+}
+
+template <typename T, int L, int NB, bool FPF = false>
 struct TmaColCfg {
-  using CF = ColCfg<T, L, WIDE>;
   using SH = Shape<L>;
-  static constexpr int N = SH::N, B = CF::B, THREADS = CF::THREADS;
+  static constexpr int N = SH::N, B = NB, TPT = SH::TPT, THREADS = TPT * NB;
+  // resident CTAs per SM the registers are capped for: two for the narrow shape
+  static constexpr int MINB = NB < tma_cols_per_cta<T, L>(true) ? 2 : 1;
+  static constexpr int PS = SH::EB > 0 ? SH::EB : 30;
+  static constexpr int RAW = N + (N >> (PS > 20 ? 30 : PS));  // one pad word per E words
   static constexpr int BOX = N < 256 ? N : 256;   // rows per TMA box (hardware limit 256)
   static constexpr int NBOX = N / BOX;
   static constexpr int NPF = NBOX > 1 ? NBOX / 2 : 1;  // boxes of the first half
@@ -71,18 +89,19 @@ struct TmaColCfg {
   // the odd-row boxes of the parity mode (float32 rows only) are two complex
   // wider (pitch B + 2)
   static constexpr size_t XB = sizeof(cx<T>) * (size_t)BOX * (sizeof(T) == 4 ? B + 2 : B) * (NBOX - NPF);
-  // FPF exchange buffer: real words, column stride SS (one pad word per E
-  // words; B columns x QW / B threads per wavefront cover every bank once)
-  static constexpr int QWS = 128 / (int)sizeof(T);
-  static constexpr int SS = ((CF::RAW + QWS - 1) / QWS) * QWS + (QWS / B > 0 ? QWS / B : 1);
-  static constexpr size_t XS = sizeof(T) * (size_t)B * SS;
+  // exchange buffer of W-byte words (whole complex values, or real words in
+  // the FPF split exchange), column stride S: B columns x QW / B threads per
+  // wavefront cover every bank once
+  static constexpr int W = FPF ? (int)sizeof(T) : (int)sizeof(cx<T>);
+  static constexpr int QW = 128 / W;
+  static constexpr int S = ((RAW + QW - 1) / QW) * QW + (QW / B > 0 ? QW / B : 1);
+  static constexpr size_t XS = (size_t)W * B * S;
   static constexpr size_t PF = FPF ? BOXB * NPF + XB : BOXB * NPF;  // FPF: both halves (odd rows wider)
-  static constexpr size_t X = FPF ? XS : (CF::X_BYTES > XB ? CF::X_BYTES : XB);
-  static constexpr int S = FPF ? SS : CF::S;
-  static constexpr bool SPLIT = FPF ? true : CF::SPLIT;
+  static constexpr size_t X = FPF ? XS : (XS > XB ? XS : XB);
+  static constexpr bool SPLIT = FPF;
   static constexpr int TW = SH::TW > 0 ? SH::TW : 1;
   static constexpr size_t SMEM = PF + X + sizeof(cx<T>) * TW + 64;
-  static constexpr bool OK = CF::CL == 1 && CF::GROUPS == 1 && CF::XCHG && SMEM <= 227 * 1024 &&
+  static constexpr bool OK = SH::P > 1 && SMEM * MINB <= 227 * 1024 && THREADS <= 1024 &&
                              B * sizeof(cx<T>) <= 256 && (NBOX == 1 || 2 * NPF == NBOX) && SH::TPT % 2 == 0;
 };
 
@@ -112,18 +131,13 @@ struct TmaColParams {
                          // through TMA boxes staged in the drained exchange buffer, the rest through STG
 };
 
-// resident CTAs per SM the TMA column kernel is compiled for (register cap)
-#ifndef TFFFT_TMA_MINB
-#define TFFFT_TMA_MINB 1
-#endif
-template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
-__global__ void __launch_bounds__(ColCfg<T, L, WIDE>::THREADS, TFFFT_TMA_MINB)
+template <typename T, int L, bool INV, int NB, bool TWO, bool FPF>
+__global__ void __launch_bounds__(TmaColCfg<T, L, NB, FPF>::THREADS, TmaColCfg<T, L, NB, FPF>::MINB)
 col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map_odd,
                const TmaColParams prm) {
-  using TC = TmaColCfg<T, L, WIDE, FPF>;
-  using CF = ColCfg<T, L, WIDE>;
+  using TC = TmaColCfg<T, L, NB, FPF>;
   using SH = Shape<L>;
-  using ST = Stockham<T, L, INV, TC::S, CF::PS, TC::SPLIT, 0, true>;
+  using ST = Stockham<T, L, INV, TC::S, TC::PS, TC::SPLIT, 0, true>;
   constexpr int E = SH::E, TPT = SH::TPT, B = TC::B, BOX = TC::BOX, N = SH::N;
   static_assert(TC::OK, "unsupported column-kernel shape for the TMA path");
   static_assert(BOX % TPT == 0, "a thread's operand rows tt + TPT kk stay inside box (TPT kk) / BOX");
@@ -306,7 +320,7 @@ __host__ __device__ constexpr bool col_tma_supported(int L) { return L == 9 || L
 template <typename T>
 cudaError_t launch_col_tma(int L, bool inv, bool wide, bool two, const CUtensorMap& map, const CUtensorMap& map_odd,
                            const TmaColParams& p, cudaStream_t s);
-// the full-prefetch variant is the default for WIDE passes (TFFFT_TMA_FPF=0 disables it, launch_col_tma)
+// the full-prefetch variant is the default (TFFFT_TMA_FPF=0 disables it, launch_col_tma)
 // columns per tile (the box width) of the TMA column kernel
 template <typename T>
 int col_tma_width(int L, bool wide);

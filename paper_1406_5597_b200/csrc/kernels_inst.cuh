@@ -267,18 +267,18 @@ cudaError_t launch_fourstep_tma<TFFFT_REAL>(int L, bool inv, const CUtensorMap* 
   }
 }
 
-template <typename T, int L, bool INV, bool WIDE, bool TWO, bool FPF>
+template <typename T, int L, bool INV, int NB, bool TWO, bool FPF>
 static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, const TmaColParams& p, cudaStream_t s) {
-  using TC = TmaColCfg<T, L, WIDE, FPF>;
+  using TC = TmaColCfg<T, L, NB, FPF>;
   if constexpr (!TC::OK) {
     return cudaErrorNotSupported;  // col_tma_width() reports 0 for this shape: never launched
   } else {
-  auto k = col_tma_kernel<T, L, INV, WIDE, TWO, FPF>;
+  auto k = col_tma_kernel<T, L, INV, NB, TWO, FPF>;
   static KernelCache kc;
   const cudaError_t prep = prep_smem(k, kc, TC::SMEM);
   if (prep != cudaSuccess) return prep;
   if (p.ntiles <= 0) return cudaSuccess;
-  // persistent: every resident CTA slot of the GPU (one per SM at 216 registers)
+  // persistent: every resident CTA slot of the GPU (one per SM wide, two narrow)
   const long long blocks =
       std::min<long long>(p.ntiles, (long long)occupancy(k, kc, TC::THREADS, TC::SMEM) * num_sms());
   (void)cudaGetLastError();
@@ -287,11 +287,11 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
   }
 }
 
-// full-prefetch variant (col_tma.cuh FPF), the default for the WIDE (128-byte
-// row) column passes; TFFFT_TMA_FPF=0 selects the half-and-half prefetch.
-// Measured at 1024^3 (profiles/r02/fpf_ab.txt): isolated (ncu) 3.00 vs 2.97 ms
-// per launch, but in the live pair at the power cap stage 3 + 3' take
-// 6.61-6.76 ms instead of 7.00-7.05 (float32: 3.31 vs 3.43 ms).
+// full-prefetch variant (col_tma.cuh FPF), the default; TFFFT_TMA_FPF=0
+// selects the half-and-half prefetch.  Measured at 1024^3
+// (profiles/r02/fpf_ab.txt): isolated (ncu) 3.00 vs 2.97 ms per launch, but in
+// the live pair at the power cap stage 3 + 3' take 6.61-6.76 ms instead of
+// 7.00-7.05 (float32: 3.31 vs 3.43 ms).
 static bool tma_fpf() {
   static const bool v = [] {
     const char* e = getenv("TFFFT_TMA_FPF");
@@ -299,19 +299,33 @@ static bool tma_fpf() {
   }();
   return v;
 }
+// narrow shape (half-width tiles, two CTAs per SM) for the stage-1b passes:
+// TFFFT_TMA_NARROW=1.  Measured on one box (profiles/r02/narrow_ab.txt):
+// 2.96 vs 2.86 ms per isolated 1024^3 stage-1b launch and no gain in the live
+// pair, so the wide shape is the default everywhere.
+static bool tma_narrow() {
+  static const bool v = [] {
+    const char* e = getenv("TFFFT_TMA_NARROW");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
+template <typename T, int L, bool TWO, int NB>
+static cudaError_t tc_dispatch3(bool inv, const CUtensorMap& map, const CUtensorMap& map_odd, const TmaColParams& p,
+                                cudaStream_t s) {
+  if (tma_fpf() && TmaColCfg<T, L, NB, true>::OK)
+    return inv ? tc_one<T, L, true, NB, TWO, true>(map, map_odd, p, s)
+               : tc_one<T, L, false, NB, TWO, true>(map, map_odd, p, s);
+  return inv ? tc_one<T, L, true, NB, TWO, false>(map, map_odd, p, s)
+             : tc_one<T, L, false, NB, TWO, false>(map, map_odd, p, s);
+}
 
 template <typename T, int L, bool TWO>
 static cudaError_t tc_dispatch2(bool inv, bool wide, const CUtensorMap& map, const CUtensorMap& map_odd,
                                 const TmaColParams& p, cudaStream_t s) {
-  if (wide) {
-    if (tma_fpf() && TmaColCfg<T, L, true, true>::OK)
-      return inv ? tc_one<T, L, true, true, TWO, true>(map, map_odd, p, s)
-                 : tc_one<T, L, false, true, TWO, true>(map, map_odd, p, s);
-    return inv ? tc_one<T, L, true, true, TWO, false>(map, map_odd, p, s)
-               : tc_one<T, L, false, true, TWO, false>(map, map_odd, p, s);
-  }
-  return inv ? tc_one<T, L, true, false, TWO, false>(map, map_odd, p, s)
-             : tc_one<T, L, false, false, TWO, false>(map, map_odd, p, s);
+  if (wide || !tma_narrow()) return tc_dispatch3<T, L, TWO, tma_cols_per_cta<T, L>(true)>(inv, map, map_odd, p, s);
+  return tc_dispatch3<T, L, TWO, tma_cols_per_cta<T, L>(false)>(inv, map, map_odd, p, s);
 }
 
 template <typename T, int L>
@@ -333,12 +347,12 @@ cudaError_t launch_col_tma<TFFFT_REAL>(int L, bool inv, bool wide, bool two, con
 
 template <>
 int col_tma_width<TFFFT_REAL>(int L, bool wide) {
+  const bool w = wide || !tma_narrow();
+  constexpr int W9 = tma_cols_per_cta<TFFFT_REAL, 9>(true), N9 = tma_cols_per_cta<TFFFT_REAL, 9>(false);
+  constexpr int W10 = tma_cols_per_cta<TFFFT_REAL, 10>(true), N10 = tma_cols_per_cta<TFFFT_REAL, 10>(false);
   switch (L) {
-    case 9: return wide ? (TmaColCfg<TFFFT_REAL, 9, true>::OK ? TmaColCfg<TFFFT_REAL, 9, true>::B : 0)
-                        : (TmaColCfg<TFFFT_REAL, 9, false>::OK ? TmaColCfg<TFFFT_REAL, 9, false>::B : 0);
-    case 10: return wide ? (TmaColCfg<TFFFT_REAL, 10, true>::OK ? TmaColCfg<TFFFT_REAL, 10, true>::B : 0)
-                         : (TmaColCfg<TFFFT_REAL, 10, false>::OK ? TmaColCfg<TFFFT_REAL, 10, false>::B : 0);
-    // (the full-prefetch variant has the same box width)
+    case 9: return w ? (TmaColCfg<TFFFT_REAL, 9, W9>::OK ? W9 : 0) : (TmaColCfg<TFFFT_REAL, 9, N9>::OK ? N9 : 0);
+    case 10: return w ? (TmaColCfg<TFFFT_REAL, 10, W10>::OK ? W10 : 0) : (TmaColCfg<TFFFT_REAL, 10, N10>::OK ? N10 : 0);
     default: return 0;
   }
 }

@@ -470,6 +470,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
 struct TwoLevelJob {
+  bool wide;  // stage 3 / 3' (128-byte row segments) or stage 1b / 1b' (narrow CTA shape)
   const void* ld_base;
   long long cols, ngrp;
   long long ld_in_rows, ld_blocks, ld_in, ld_out, ld_g;
@@ -518,7 +519,8 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
 #endif
   if (rd == 0 && c.grp_stride != 0) {
     bool done = false;
-    TRY(columns_tma(pl, pl->L1, inv, true, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
+    // stage 1b: rows n2c elements apart, the narrow CTA shape (two per SM)
+    TRY(columns_tma(pl, pl->L1, inv, false, c.data, pl->n2c, nplanes, pl->n2c, (long long)pl->n1 * pl->n2c,
                     pl->tw1, s, &done));
     if (done) return TFFFT_OK;
   } else if (rd != 0) {
@@ -527,6 +529,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
     const BufSet& B = pl->bs[pl->cur];
     const long long n1p = pl->n1p, n2c = pl->n2c, band = (long long)pl->n0p * n1p * n2c;
     TwoLevelJob j{};
+    j.wide = false;
     j.cols = n2c;
     j.ngrp = nplanes;
     if (!inv) {
@@ -672,7 +675,7 @@ static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& 
   if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
       reinterpret_cast<uintptr_t>(j.ld_base) % 16)
     return TFFFT_OK;
-  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, true) : col_tma_width<float>(L, true);
+  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, j.wide) : col_tma_width<float>(L, j.wide);
   if (B <= 0 || j.ld_in_rows * j.ld_blocks != n) return TFFFT_OK;
   const long long brows = std::min<long long>(std::min<long long>(n, 256), j.ld_in_rows);
   CUtensorMap map;
@@ -713,8 +716,8 @@ static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& 
   }
   w.evict_first = (j.ld_in * esz) % 128 == 0;
   pl->launches++;
-  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, true, two, map, map, w, s)
-                                               : launch_col_tma<float>(L, inv, true, two, map, map, w, s);
+  const cudaError_t e = pl->dtype == TFFFT_F64 ? launch_col_tma<double>(L, inv, j.wide, two, map, map, w, s)
+                                               : launch_col_tma<float>(L, inv, j.wide, two, map, map, w, s);
   CUDA_TRY(e);
   *done = true;
   return TFFFT_OK;
@@ -834,6 +837,7 @@ static int stage3_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s)
     const BufSet& B = pl->bs[pl->cur];
     const long long n1p = pl->n1p, n2c = pl->n2c, band = (long long)pl->n0p * n1p * n2c;
     TwoLevelJob j{};
+    j.wide = true;
     j.cols = n1p * n2c;
     j.ngrp = 1;
     j.ld_in_rows = pl->n0p;
@@ -1916,7 +1920,17 @@ static int pipeline(tffft_plan_t pl, cudaStream_t s, Produce produce, Consume co
       const int st = c & 1;
       pl->cur = st;
       if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[st], 0));
-      TRY(guard_outgoing(pl, s));
+      if (!fabric_kind(pl) && pl->peer_stores) {
+        // NCCL: the guard barrier goes on the exchange stream too, so every NCCL
+        // operation of the communicator is issued on one stream in one order
+        CUDA_TRY(cudaEventRecord(pl->ev_s3[st], s));
+        CUDA_TRY(cudaStreamWaitEvent(x, pl->ev_s3[st], 0));
+        TRY(guard_outgoing(pl, x));
+        CUDA_TRY(cudaEventRecord(pl->ev_x[st], x));
+        CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[st], 0));
+      } else {
+        TRY(guard_outgoing(pl, s));
+      }
       TRY(produce(c));
       CUDA_TRY(cudaEventRecord(pl->ev_s1[st], s));
       CUDA_TRY(cudaStreamWaitEvent(x, pl->ev_s1[st], 0));
