@@ -111,9 +111,13 @@ enum {
   TFFFT_FLAG_PEER_STORES = 8,     /* fused exchange: the stage-1 / stage-3' epilogues store every peer band
                                      straight into the peer's landing buffer (peer memory), and the
                                      exchange reduces to a barrier.  Local fabric communicators. */
-  TFFFT_FLAG_TMA_COLUMNS = 16     /* p = 1 column passes of length 512 / 1024 fed by TMA box copies
-                                     (col_tma.cuh), the default (flags < 0) unless TFFFT_TMA_COLS=0;
-                                     explicit flags without it select the cp.async column kernel */
+  TFFFT_FLAG_CHUNKED_EXCHANGE = 32, /* p > 1 forward: stage 1 in plane chunks, each chunk's part of every band
+                                     exchanged (on the plan's exchange stream) while the next chunk computes;
+                                     the default on NCCL communicators (TFFFT_XCHUNKS chunks, default 4),
+                                     opt-in on the local fabric and IPC */
+  TFFFT_FLAG_TMA_COLUMNS = 16     /* column passes of length 512 / 1024 fed by TMA box copies (col_tma.cuh,
+                                     any p), the default (flags < 0) unless TFFFT_TMA_COLS=0; explicit
+                                     flags without it select the cp.async column kernel */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

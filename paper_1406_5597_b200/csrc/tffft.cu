@@ -276,6 +276,7 @@ struct tffft_plan_s {
   BufSet bs[2];
   int nsets = 1;
   int cur = 0;               // the set the stage launchers address
+  int xchunks = 1;           // plane chunks of the chunked forward exchange (1 = one exchange per call)
   bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
   bool peer_stores_wanted = false;  // NCCL communicator: peer stores once the peers' landing buffers are attached
   std::vector<void*> ipc_opened;    // peer mappings opened through CUDA IPC (closed at destroy)
@@ -426,11 +427,11 @@ static cudaError_t c2r_launch(tffft_plan_t pl, const RowParams& prm, cudaStream_
 
 // local-fabric pull: chunk c copies `words` W-sized words from ptrs[2c] to ptrs[2c+1]
 template <typename W>
-__global__ void pull_chunks_kernel(void* const* __restrict__ ptrs, long long words, int nchunks) {
+__global__ void pull_chunks_kernel(void* const* __restrict__ ptrs, long long off, long long words, int nchunks) {
   const int c = blockIdx.y;
   if (c >= nchunks) return;
-  const W* __restrict__ src = reinterpret_cast<const W*>(ptrs[2 * c]);
-  W* __restrict__ dst = reinterpret_cast<W*>(ptrs[2 * c + 1]);
+  const W* __restrict__ src = reinterpret_cast<const W*>(ptrs[2 * c]) + off;
+  W* __restrict__ dst = reinterpret_cast<W*>(ptrs[2 * c + 1]) + off;
   for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words;
        w += (long long)gridDim.x * blockDim.x)
     dst[w] = src[w];
@@ -483,7 +484,8 @@ static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& 
 
 // stage 1b / 1b': c2c along n1 of every (plane i, bin k) column of `nplanes`
 // planes starting at `spec` (a batched p = 1 plan passes all batch * n0p planes)
-static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int nplanes) {
+// (plane0: the first plane's index within the field, for the band redirects)
+static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s, int nplanes, int plane0 = 0) {
   ColParams c{};
   c.data = spec;
   c.tw = pl->tw1;
@@ -509,7 +511,7 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
     c.stg_band = (long long)pl->n0p * pl->n1p * pl->n2c;
     c.stg_within = pl->n2c;
     c.stg_grp = (long long)pl->n1p * pl->n2c;
-    c.stg_base = 0;
+    c.stg_base = (long long)plane0 * c.stg_grp;
   }
 #if TFFFT_PROBES
   {  // profiling probe: every plane aliases plane 0 (same work, L2-resident footprint)
@@ -534,7 +536,8 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
     j.ngrp = nplanes;
     if (!inv) {
       j.ld_base = spec; j.ld_in_rows = pl->n1; j.ld_blocks = 1; j.ld_in = n2c; j.ld_g = (long long)pl->n1 * n2c;
-      j.st_tab = B.band_dst_h; j.st_rows = n1p; j.st_in = n2c; j.st_g = n1p * n2c;
+      for (void* d : B.band_dst_h) j.st_tab.push_back(static_cast<char*>(d) + (size_t)plane0 * n1p * n2c * pl->esz);
+      j.st_rows = n1p; j.st_in = n2c; j.st_g = n1p * n2c;
     } else {
       j.ld_base = B.landing; j.ld_in_rows = n1p; j.ld_blocks = pl->p; j.ld_in = n2c; j.ld_out = band;
       j.ld_g = n1p * n2c;
@@ -922,10 +925,6 @@ static int stage1_fused(tffft_plan_t pl, void* real, void* spec, bool fwd, cudaS
   return TFFFT_OK;
 }
 
-static uint64_t wire_bytes(tffft_plan_t pl) {
-  return (uint64_t)(pl->p - 1) * pl->n0p * pl->n1p * pl->n2c * pl->esz;
-}
-
 static size_t band_bytes(tffft_plan_t pl) { return (size_t)pl->n0p * pl->n1p * pl->n2c * pl->esz; }
 
 // Stream-ordered barrier over an NCCL communicator: a one-int all-reduce.  It
@@ -1021,30 +1020,39 @@ static int nccl_async_check(tffft_comm_t c) {
   return TFFFT_OK;
 }
 
-static int launch_pull(tffft_plan_t pl, void* const* ptrs, int nchunks, cudaStream_t s) {
-  const long long bytes = (long long)band_bytes(pl);
-  const bool wide = bytes % 16 == 0;
-  const long long words = wide ? bytes / 16 : bytes / 8;
+// pull rows [i0, i0 + ni) of each listed band (the whole band: i0 = 0, ni = n0p)
+static int launch_pull(tffft_plan_t pl, void* const* ptrs, int nchunks, cudaStream_t s, long long i0 = 0,
+                       long long ni = -1) {
+  if (ni < 0) ni = pl->n0p;
+  const long long row = (long long)pl->n1p * pl->n2c * (long long)pl->esz;  // bytes of one plane's chunk
+  const bool wide = row % 16 == 0;
+  const long long wb = wide ? 16 : 8;
+  const long long words = ni * row / wb, off = i0 * row / wb;
   dim3 grid((unsigned)std::min<long long>((words + 255) / 256, 2048), (unsigned)nchunks);
   if (wide)
-    pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(ptrs, words, nchunks);
+    pull_chunks_kernel<int4><<<grid, 256, 0, s>>>(ptrs, off, words, nchunks);
   else
-    pull_chunks_kernel<int2><<<grid, 256, 0, s>>>(ptrs, words, nchunks);
+    pull_chunks_kernel<int2><<<grid, 256, 0, s>>>(ptrs, off, words, nchunks);
   pl->launches++;
   CUDA_TRY(cudaGetLastError());
   return TFFFT_OK;
 }
 
-static int exchange(tffft_plan_t pl, cudaStream_t s) {
+// i0 / ni: the planes of every band this exchange moves (default: all; the
+// chunked forward moves plane chunks as stage 1 produces them)
+static int exchange(tffft_plan_t pl, cudaStream_t s, long long i0 = 0, long long ni = -1) {
   if (pl->p == 1) return TFFFT_OK;
   TRY(nccl_async_check(pl->comm));
   BufSet& B = pl->bs[pl->cur];
+  if (ni < 0) ni = pl->n0p;
   const long long band = (long long)pl->n0p * pl->n1p * pl->n2c;  // complex elements per peer
+  const long long chunk = (long long)pl->n1p * pl->n2c;            // complex elements per plane of a band
+  const uint64_t wire = (uint64_t)(pl->p - 1) * ni * chunk * pl->esz;
   if (pl->peer_stores && !fabric_kind(pl)) {
     // the epilogue already stored every band into its peer's landing buffer
     // over NVLink (CUDA IPC mapping): the exchange is the barrier
     TRY(nccl_barrier(pl, s));
-    pl->counters[1] += wire_bytes(pl);
+    pl->counters[1] += wire;
     return TFFFT_OK;
   }
   if (pl->peer_stores) {
@@ -1054,7 +1062,7 @@ static int exchange(tffft_plan_t pl, cudaStream_t s) {
     TRY(pl->comm->barrier());
     for (int q = 0; q < pl->p; ++q)
       if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, B.ready[q], 0));
-    pl->counters[1] += wire_bytes(pl);
+    pl->counters[1] += wire;
     return TFFFT_OK;
   }
   if (!fabric_kind(pl)) {
@@ -1062,19 +1070,21 @@ static int exchange(tffft_plan_t pl, cudaStream_t s) {
     const ncclDataType_t dt = pl->dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
     char* stg = static_cast<char*>(B.staging);
     char* lnd = static_cast<char*>(B.landing);
-    if (pl->pattern == TFFFT_COLLECTIVE && api.AlltoAll) {
+    if (pl->pattern == TFFFT_COLLECTIVE && api.AlltoAll && ni == pl->n0p) {
       // COLLECTIVE (transport.py:395-419): every rank deposits all of its
       // outgoing bands in one all-to-all; the self slot carries the self band
       // from staging[rank] to landing[rank] (build_band_dst)
       NCCL_TRY(api.AlltoAll(stg, lnd, 2 * band, dt, pl->comm->nccl, s));
-      pl->counters[1] += wire_bytes(pl);
+      pl->counters[1] += wire;
       return TFFFT_OK;
     }
+    // one send and one receive per peer (the plane range of each band is contiguous)
+    const long long off = i0 * chunk * pl->esz, count = 2 * ni * chunk;
     NCCL_TRY(api.GroupStart());
     for (int d = 1; d < pl->p; ++d) {
       const int to = (pl->rank + d) % pl->p, from = (pl->rank - d + pl->p) % pl->p;
-      NCCL_TRY(api.Send(stg + (long long)to * band * pl->esz, 2 * band, dt, to, pl->comm->nccl, s));
-      NCCL_TRY(api.Recv(lnd + (long long)from * band * pl->esz, 2 * band, dt, from, pl->comm->nccl, s));
+      NCCL_TRY(api.Send(stg + (long long)to * band * pl->esz + off, count, dt, to, pl->comm->nccl, s));
+      NCCL_TRY(api.Recv(lnd + (long long)from * band * pl->esz + off, count, dt, from, pl->comm->nccl, s));
     }
     NCCL_TRY(api.GroupEnd());
   } else {
@@ -1088,14 +1098,14 @@ static int exchange(tffft_plan_t pl, cudaStream_t s) {
     for (int q = 0; q < pl->p; ++q)
       if (q != pl->rank) CUDA_TRY(cudaStreamWaitEvent(s, B.ready[q], 0));
     if (pl->pattern == TFFFT_COLLECTIVE) {
-      TRY(launch_pull(pl, B.pull_ptrs, pl->p - 1, s));
+      TRY(launch_pull(pl, B.pull_ptrs, pl->p - 1, s, i0, ni));
     } else {
-      for (int d = 1; d < pl->p; ++d) TRY(launch_pull(pl, B.pull_ptrs + 2 * (d - 1), 1, s));
+      for (int d = 1; d < pl->p; ++d) TRY(launch_pull(pl, B.pull_ptrs + 2 * (d - 1), 1, s, i0, ni));
     }
     CUDA_TRY(cudaEventRecord(B.done[pl->rank], s));
     TRY(pl->comm->barrier());
   }
-  pl->counters[1] += wire_bytes(pl);
+  pl->counters[1] += wire;
   return TFFFT_OK;
 }
 
@@ -1395,7 +1405,7 @@ int tffft_plan_flags(tffft_plan_t pl, int* flags) {
   if (!pl || !flags) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   *flags = (pl->s1_fused ? TFFFT_FLAG_FUSED_STAGE1 : 0) | (pl->fs_la > 0 ? TFFFT_FLAG_FOURSTEP_STAGE3 : 0) |
            (pl->strategy == 1 ? TFFFT_FLAG_TRANSPOSE : 0) | (pl->peer_stores ? TFFFT_FLAG_PEER_STORES : 0) |
-           (pl->tma_cols == 1 ? TFFFT_FLAG_TMA_COLUMNS : 0);
+           (pl->tma_cols == 1 ? TFFFT_FLAG_TMA_COLUMNS : 0) | (pl->xchunks > 1 ? TFFFT_FLAG_CHUNKED_EXCHANGE : 0);
   return TFFFT_OK;
 }
 
@@ -1607,7 +1617,7 @@ int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, in
         B.own_events = true;
       }
     }
-    if (pl->nsets > 1) {
+    {  // exchange stream + hand-off events: batched pipeline, chunked forward
       CUDA_TRY(cudaStreamCreateWithFlags(&pl->xstream, cudaStreamNonBlocking));
       for (int st = 0; st < 2; ++st) {
         CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_s1[st], cudaEventDisableTiming));
@@ -1616,6 +1626,16 @@ int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, in
       }
     }
     const bool ps = (flags & TFFFT_FLAG_PEER_STORES) && strategy == 0;
+    // chunked forward exchange: on NCCL by default (the NVLink transfer of
+    // plane chunk c overlaps stage 1 of chunk c+1), opt-in on the fabrics
+    if (strategy == 0 && !ps && pl->nsets == 1 && pl->n0p >= 2 &&
+        ((flags & TFFFT_FLAG_CHUNKED_EXCHANGE) || comm->kind == COMM_NCCL)) {
+      static const int env = [] {
+        const char* e = getenv("TFFFT_XCHUNKS");
+        return e ? atoi(e) : 0;
+      }();
+      pl->xchunks = std::max(1, std::min(env > 0 ? env : 4, pl->n0p));
+    }
     if (comm->kind == COMM_LOCAL) {
       pl->seq = comm->plan_seq++;
       pl->peer_stores = ps;
@@ -1901,6 +1921,42 @@ static int inverse_field(tffft_plan_t pl, void* spec, void* real, int nf, int c,
   return TFFFT_OK;
 }
 
+// Chunked forward at p > 1 (one field): stage 1 runs plane chunk after plane
+// chunk on the caller's stream s; each chunk's part of every band is exchanged
+// on the exchange stream x as soon as the chunk is produced, so the transfer
+// of chunk c overlaps stage 1 of chunk c+1 (a band's plane range is contiguous
+// in staging and landing).  Stage 3 waits for the last chunk.
+static int forward_chunked(tffft_plan_t pl, const void* real, void* spec, cudaStream_t s, StageEvents* ev) {
+  cudaStream_t x = pl->xstream;
+  pl->cur = 0;
+  TRY(guard_outgoing(pl, s));
+  const int C = pl->xchunks, m = (pl->n0p + C - 1) / C;
+  const size_t rb = (size_t)pl->n1 * pl->n2 * (pl->esz / 2), sb = (size_t)pl->n1 * pl->n2c * pl->esz;
+  {
+    NvtxRange r("stage1+exchange");
+    for (int a = 0, k = 0; a < pl->n0p; a += m, ++k) {
+      const int cnt = std::min(m, pl->n0p - a);
+      char* sp = static_cast<char*>(spec) + (size_t)a * sb;
+      CUDA_TRY(r2c_launch(pl, row_params(pl, const_cast<char*>(static_cast<const char*>(real) + (size_t)a * rb), sp,
+                                         cnt, a), s));
+      TRY(stage1_columns(pl, sp, false, s, cnt, a));
+      CUDA_TRY(cudaEventRecord(pl->ev_s1[k & 1], s));
+      CUDA_TRY(cudaStreamWaitEvent(x, pl->ev_s1[k & 1], 0));
+      TRY(exchange(pl, x, a, cnt));
+    }
+    CUDA_TRY(cudaEventRecord(pl->ev_x[0], x));
+    CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[0], 0));
+  }
+  MARK(ev, 1, s);
+  MARK(ev, 2, s);
+  {
+    NvtxRange r("stage3");
+    TRY(stage3_columns(pl, spec, false, s));
+  }
+  MARK(ev, 3, s);
+  return TFFFT_OK;
+}
+
 // Batched p > 1 (STRIDED): a two-deep software pipeline over the fields.  The
 // stages run on the caller's stream s, the exchanges on the plan's exchange
 // stream x; field c uses buffer set c % 2, so field c's exchange overlaps
@@ -1974,7 +2030,10 @@ int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* st
       StageEvents* ev;
       TRY(begin_events(pl, true, s, &ev));
       pl->cur = 0;
-      TRY(forward_field(pl, real + c * real_bytes(pl), spec + c * spec_bytes(pl), 1, s, ev));
+      if (pl->xchunks > 1)
+        TRY(forward_chunked(pl, real + c * real_bytes(pl), spec + c * spec_bytes(pl), s, ev));
+      else
+        TRY(forward_field(pl, real + c * real_bytes(pl), spec + c * spec_bytes(pl), 1, s, ev));
     }
     return TFFFT_OK;
   }

@@ -122,7 +122,8 @@ class FftPlan:
             pass
 
 
-ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8, "tma_columns": 16}
+ALGORITHM_FLAGS = {"fused_stage1": 1, "fourstep_stage3": 2, "peer_stores": 8, "tma_columns": 16,
+                   "chunked_exchange": 32}
 TRANSPOSE_FLAG = 4
 
 
@@ -141,7 +142,8 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     NCCL (peer stores) / IPC communicators, whose buffers are exchanged here.
 
     ``algorithms`` selects optional kernel schedules ("fused_stage1",
-    "fourstep_stage3", "peer_stores", "tma_columns"); None takes the library
+    "fourstep_stage3", "peer_stores", "tma_columns", "chunked_exchange");
+    None takes the library
     defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS environment
     switches; by default the 512- and 1024-point column passes at p = 1 are
     TMA-fed).  ``batch`` > 1 makes a batched plan: ``forward_many`` /

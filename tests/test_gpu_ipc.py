@@ -42,6 +42,8 @@ CASES = [
     ((64, 32, 8), "PAIRWISE", None, 3),
     ((64, 32, 8), "COLLECTIVE", ("peer_stores",), 3),
     ((16, 1024, 8), "PAIRWISE", None, 1),
+    ((64, 32, 16), "PAIRWISE", ("chunked_exchange", "tma_columns"), 1),
+    ((64, 32, 16), "COLLECTIVE", ("chunked_exchange",), 1),
 ]
 
 

@@ -34,6 +34,7 @@ CASES = [
     ((256, 128, 32), 4, {"algorithms": ()}),                             # cp.async column kernel
     ((64, 64, 32), 4, {"batch": 3}),                                     # batched pipeline, 2 buffer sets
     ((512, 32, 16), 2, {"batch": 4, "algorithms": ("peer_stores", "tma_columns")}),
+    ((1024, 32, 16), 4, {"algorithms": ("chunked_exchange", "tma_columns")}),      # plane-chunked forward
 ]
 
 
