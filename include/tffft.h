@@ -184,6 +184,13 @@ int tffft_consistency(tffft_plan_t plan, double* residue);
  * records with 0xFF bytes (NaN), so a read of an element no stage wrote shows
  * up as NaN in the output; synchronous */
 int tffft_plan_poison(tffft_plan_t plan);
+/* Deferred consistency mode (deferred = 1): every inverse folds its Hermitian
+ * check (the same test as tffft_consistency) into a device accumulator, with no
+ * host synchronisation per call; tffft_consistency_collect synchronises,
+ * returns the largest residue and TFFFT_ERR_CONSISTENCY if any inverse since
+ * the last collect violated the tolerance.  deferred = 0: tffft_consistency. */
+int tffft_set_consistency_mode(tffft_plan_t plan, int deferred);
+int tffft_consistency_collect(tffft_plan_t plan, double* residue, uint64_t* calls);
 /* number of kernels this library launched on the plan since the last reset */
 int tffft_launch_count(tffft_plan_t plan, uint64_t* launches);
 

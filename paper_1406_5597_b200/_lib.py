@@ -56,6 +56,8 @@ _SIGS = {
     "tffft_counters": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_uint64)]),
     "tffft_reset_instrumentation": (_c.c_int, [_c.c_void_p]),
     "tffft_consistency": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_double)]),
+    "tffft_set_consistency_mode": (_c.c_int, [_c.c_void_p, _c.c_int]),
+    "tffft_consistency_collect": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_double), _c.POINTER(_c.c_uint64)]),
     "tffft_launch_count": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_uint64)]),
     "tffft_exchange_schedule": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int,
                                            _c.POINTER(_c.c_int64), _c.c_int64, _c.POINTER(_c.c_int64)]),

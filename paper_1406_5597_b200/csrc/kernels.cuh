@@ -656,6 +656,29 @@ static __global__ void __launch_bounds__(256) reduce_row_stats_kernel(const doub
   }
 }
 
+// Deferred Hermitian check: fold the per-plane statistics of one inverse into
+// a device accumulator, with the host's test (kernels.py:222-238: |Im X_0|,
+// |Im X_N| and the residue against rtol * n2 * max|X|), so a run of inverses
+// needs no host synchronisation per call.  acc: [0] max residue, [1]
+// violations, [2] first violating plane (field-major index), [3] worst
+// max(edge, residue) / tol -- non-negative doubles compared as integers.
+static __global__ void __launch_bounds__(256) consistency_fold_kernel(const unsigned long long* stats, int planes,
+                                                                      double n2, double rtol,
+                                                                      unsigned long long* acc) {
+  for (int i = threadIdx.x; i < planes; i += blockDim.x) {
+    const double m2 = __longlong_as_double((long long)stats[3 * i]);
+    const double edge = __longlong_as_double((long long)stats[3 * i + 1]);
+    const double r = __longlong_as_double((long long)stats[3 * i + 2]);
+    const double tol = rtol * n2 * sqrt(m2);
+    atomicMax(acc + 0, ord(r));
+    if (edge > tol || r > tol) {
+      atomicAdd(acc + 1, 1ull);
+      atomicMin(acc + 2, (unsigned long long)i);
+      atomicMax(acc + 3, ord(fmax(edge, r) / fmax(tol, 1e-300)));
+    }
+  }
+}
+
 // host-side launchers (defined in kernels_f64.cu / kernels_f32.cu)
 // variant: 0 = single stride, 1 = single stride + redirect, 2 = two-level, 3 = two-level + redirect
 // wide: stage-3 tiles (128-byte row visits for either precision); two: two-level

@@ -317,6 +317,9 @@ struct tffft_plan_s {
   uint64_t launches = 0;
   cudaStream_t last_inverse_stream = nullptr;
   bool inverse_ran = false;
+  bool deferred_check = false;          // fold every inverse's Hermitian check on the device
+  unsigned long long* check_acc = nullptr;  // consistency_fold_kernel accumulator (4 words)
+  uint64_t deferred_calls = 0;
 };
 
 static bool pow2(long long n) { return n >= 1 && (n & (n - 1)) == 0; }
@@ -1758,6 +1761,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaFree(pl->s1_counters);
   cudaFree(pl->col_ticket);
   cudaFree(pl->barrier_word);
+  cudaFree(pl->check_acc);
   delete pl;
   return TFFFT_OK;
 }
@@ -2087,8 +2091,64 @@ int tffft_inverse(tffft_plan_t pl, void* spec_inout, void* real_out, void* strea
         [&](int c) { return inv_stage1(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), 1, c, s); }));
     MARK(ev, 3, s);
   }
+  if (pl->deferred_check) {  // the Hermitian check of this call, folded on the device
+    if (!pl->s1_fused) {
+      reduce_row_stats_kernel<<<pl->n0p * pl->batch, 256, 0, s>>>(pl->row_stats, pl->n1, pl->stats);
+      pl->launches++;
+    }
+    consistency_fold_kernel<<<1, 256, 0, s>>>(pl->stats, pl->n0p * pl->batch, (double)pl->n2,
+                                              pl->dtype == TFFFT_F64 ? 1e-9 : 1e-4, pl->check_acc);
+    pl->launches++;
+    CUDA_TRY(cudaGetLastError());
+    pl->deferred_calls++;
+  }
   pl->last_inverse_stream = s;
   pl->inverse_ran = true;
+  return TFFFT_OK;
+}
+
+static int reset_check_acc(tffft_plan_t pl, cudaStream_t s) {
+  const unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
+  CUDA_TRY(cudaMemcpyAsync(pl->check_acc, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return TFFFT_OK;
+}
+
+// Deferred consistency (mode 1): every inverse folds its Hermitian check into
+// a device accumulator instead of waiting for tffft_consistency; the verdict
+// of all inverses since the last collect is read by tffft_consistency_collect.
+int tffft_set_consistency_mode(tffft_plan_t pl, int deferred) {
+  if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  if (deferred && !pl->check_acc) CUDA_TRY(cudaMalloc(&pl->check_acc, 4 * sizeof(unsigned long long)));
+  if (deferred) TRY(reset_check_acc(pl, nullptr));
+  pl->deferred_check = deferred != 0;
+  pl->deferred_calls = 0;
+  return TFFFT_OK;
+}
+
+int tffft_consistency_collect(tffft_plan_t pl, double* residue, uint64_t* calls) {
+  if (!pl || !residue) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
+  *residue = 0.0;
+  if (calls) *calls = pl->deferred_calls;
+  if (!pl->deferred_check) return fail(TFFFT_ERR_CONFIGURATION, "the plan is not in the deferred consistency mode");
+  CUDA_TRY(cudaSetDevice(pl->comm->device));
+  if (pl->last_inverse_stream || pl->inverse_ran) CUDA_TRY(cudaStreamSynchronize(pl->last_inverse_stream));
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpy(h, pl->check_acc, sizeof(h), cudaMemcpyDeviceToHost));
+  const uint64_t n = pl->deferred_calls;
+  pl->deferred_calls = 0;
+  TRY(reset_check_acc(pl, pl->last_inverse_stream));
+  double r, ratio;
+  memcpy(&r, &h[0], 8);
+  memcpy(&ratio, &h[3], 8);
+  *residue = r;
+  if (h[1] > 0)
+    return fail(TFFFT_ERR_CONSISTENCY,
+                "bins 0 and n/2 must be real for a half spectrum: %llu plane(s) over the tolerance in %llu "
+                "inverse call(s), first at field %llu plane %llu, worst %.3g x the tolerance",
+                (unsigned long long)h[1], (unsigned long long)n, (unsigned long long)(h[2] / pl->n0p),
+                (unsigned long long)(h[2] % pl->n0p), ratio);
   return TFFFT_OK;
 }
 

@@ -104,6 +104,27 @@ class FftPlan:
         _lib.check(_lib.lib().tffft_plan_workspace_bytes(self.handle, ctypes.byref(n)))
         return int(n.value)
 
+    def set_check_consistency(self, mode: bool | str) -> None:
+        """Switch the Hermitian check between True (per call, synchronous),
+        False and "deferred" (device-side, see collect_consistency)."""
+        if mode not in (True, False, "deferred"):
+            raise ConfigurationError(f"check_consistency must be True, False or 'deferred', got {mode!r}")
+        with torch.cuda.device(self.comm.device):
+            _lib.check(_lib.lib().tffft_set_consistency_mode(self.handle, int(mode == "deferred")))
+        self.check_consistency = mode
+
+    def collect_consistency(self) -> int:
+        """Deferred consistency mode (``check_consistency="deferred"``):
+        synchronise, and raise ConsistencyError if any inverse since the last
+        collect had a non-Hermitian half spectrum (kernels.py:225-238).
+        Returns the number of inverse calls checked."""
+        res = ctypes.c_double()
+        calls = ctypes.c_uint64()
+        status = _lib.lib().tffft_consistency_collect(self.handle, ctypes.byref(res), ctypes.byref(calls))
+        self.last_imag_residue = max(self.last_imag_residue, float(res.value))
+        _lib.check(status)
+        return int(calls.value)
+
     def poison(self) -> None:
         """Debug: fill the plan's exchange buffers and row records with NaN
         (tffft_plan_poison); a stage reading an element no stage wrote then
@@ -136,7 +157,7 @@ def _spectral_tag(strategy: Strategy) -> SpectralTag:
 
 def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED,
          comm_pattern: CommPattern = CommPattern.PAIRWISE, dtype: str = "float64",
-         check_consistency: bool = True, algorithms: tuple[str, ...] | None = None,
+         check_consistency: bool | str = True, algorithms: tuple[str, ...] | None = None,
          batch: int = 1) -> FftPlan:
     """Per-rank plan (dfft.py:93-145).  Collective on a LOCAL fabric, and on
     NCCL (peer stores) / IPC communicators, whose buffers are exchanged here.
@@ -151,6 +172,8 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     over all fields at p = 1; field c's exchange overlapping field c+1's
     compute at p > 1)."""
     validate(grid, comm.p)
+    if check_consistency not in (True, False, "deferred"):
+        raise ConfigurationError(f"check_consistency must be True, False or 'deferred', got {check_consistency!r}")
     if not isinstance(batch, int) or batch < 1:
         raise ConfigurationError(f"batch must be a positive int, got {batch!r}")
     if not isinstance(comm_pattern, CommPattern):
@@ -174,6 +197,9 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
         dev = torch.device("cuda", comm.device)
         work1 = torch.empty(batch * (grid.n0 // p) * grid.n1 * grid.n2c, dtype=cdt, device=dev)
         real_out = torch.empty(batch * (grid.n0 // p) * grid.n1 * grid.n2, dtype=rdt, device=dev)
+    if check_consistency == "deferred":  # every inverse folds its check on the device
+        with torch.cuda.device(comm.device):
+            _lib.check(_lib.lib().tffft_set_consistency_mode(h, 1))
     peer_stores = flags >= 0 and bool(flags & ALGORITHM_FLAGS["peer_stores"])
     if comm.p > 1 and (comm.kind == "ipc" or (comm.kind == "nccl" and peer_stores)):
         # CUDA IPC: every rank exports its exchange buffers (and, on an IPC
@@ -235,9 +261,11 @@ def forward(fp: FftPlan, real: RealSlab, out: torch.Tensor | None = None) -> Spe
 def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) -> RealSlab:
     """Distributed inverse c2r normalised by 1/(n0 n1 n2) (dfft.py:179-215).
 
-    Collective; consumes ``spec`` in place.  With ``fp.check_consistency`` the
-    call synchronises and raises ConsistencyError for a non-Hermitian half
-    spectrum, as the reference's _c2r_rows does (kernels.py:223-238)."""
+    Collective; consumes ``spec`` in place.  With ``fp.check_consistency``
+    True the call synchronises and raises ConsistencyError for a non-Hermitian
+    half spectrum, as the reference's _c2r_rows does (kernels.py:223-238);
+    with "deferred" the same check runs on the device and is reported by
+    ``fp.collect_consistency()``."""
     if fp.batch != 1:
         raise ContractError(f"plan has batch={fp.batch}: use inverse_many")
     expected = _spectral_tag(fp.strategy)
@@ -253,7 +281,7 @@ def inverse(fp: FftPlan, spec: SpectralSlab, out: torch.Tensor | None = None) ->
         raise ContractError(f"real output needs {fp.real_out.numel()} elements, got {dst.numel()}")
     _lib.check(_lib.lib().tffft_inverse(fp.handle, ctypes.c_void_p(spec.data.data_ptr()),
                                         ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
-    if fp.check_consistency:
+    if fp.check_consistency is True:
         _check_consistency(fp)
     return RealSlab(fp.real_layout, dst)
 
@@ -302,7 +330,7 @@ def inverse_many(fp: FftPlan, spec: torch.Tensor, out: torch.Tensor | None = Non
         raise ContractError(f"real output needs {fp.real_out.numel()} elements, got {dst.numel()}")
     _lib.check(_lib.lib().tffft_inverse(fp.handle, ctypes.c_void_p(spec.data_ptr()),
                                         ctypes.c_void_p(dst.data_ptr()), _stream(fp)))
-    if fp.check_consistency:
+    if fp.check_consistency is True:
         _check_consistency(fp)
     return dst
 

@@ -5,7 +5,9 @@ every step copies that step's real slab host->device, runs the forward r2c and
 inverse c2r through libtffft and copies the result device->host.  Copies run
 on their own CUDA streams and are double-buffered, so step i+1's upload and
 step i's download (PCIe is full duplex) overlap the transforms of the
-neighbouring steps instead of serialising with them.
+neighbouring steps instead of serialising with them.  With a plan made with
+``check_consistency="deferred"`` no step waits for the host: every inverse's
+Hermitian check is folded on the device and collected once at the end.
 """
 
 from __future__ import annotations
@@ -73,3 +75,5 @@ class HostPairStream:
                 upload(i + depth)
         self.d2h.synchronize()
         torch.cuda.current_stream(dev).synchronize()
+        if fp.check_consistency == "deferred":  # every step's inverse was checked on the device
+            fp.collect_consistency()

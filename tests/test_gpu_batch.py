@@ -180,3 +180,32 @@ def test_chunked_forward_exchange(p, pattern):
         assert res[q][2] == (p - 1) * n0p * n1p * n2c * 16
     back = np.concatenate([r[1] for r in res]).reshape(shape)
     assert rel(back, x) <= 1e-12
+
+
+def test_deferred_consistency_mode():
+    """check_consistency="deferred": every inverse folds the same Hermitian test
+    on the device (no host sync per call); collect_consistency reports the
+    calls checked and raises ConsistencyError for a bad spectrum in any of them."""
+    shape = (16, 16, 16)
+    grid = tf.GlobalGrid(*shape)
+    ep = tf.make_communicators(1)[0]
+    fp = tf.plan(grid, ep, check_consistency="deferred")
+    slab = tf.scatter_real(oracle.uniform_field(shape, 4), grid, 1)[0]
+    for _ in range(3):
+        tf.inverse(fp, tf.forward(fp, slab))
+    assert fp.collect_consistency() == 3
+    assert 0.0 <= fp.last_imag_residue < 1e-9
+    spec = tf.forward(fp, slab)
+    spec.data.view(16, 16, 9)[5, 2, 8] += 1j  # a Nyquist bin of plane 5 becomes non-real
+    tf.inverse(fp, spec)  # no exception at the call
+    tf.inverse(fp, tf.forward(fp, slab))
+    with pytest.raises(tf.ConsistencyError, match="plane 5"):
+        fp.collect_consistency()
+    tf.inverse(fp, tf.forward(fp, slab))  # the accumulator was reset by the collect
+    assert fp.collect_consistency() == 1
+    fp.set_check_consistency(True)
+    spec = tf.forward(fp, slab)
+    spec.data.view(16, 16, 9)[5, 2, 8] += 1j
+    with pytest.raises(tf.ConsistencyError):
+        tf.inverse(fp, spec)
+    fp.close()
