@@ -196,10 +196,10 @@ def test_deferred_consistency_mode():
     assert fp.collect_consistency() == 3
     assert 0.0 <= fp.last_imag_residue < 1e-9
     spec = tf.forward(fp, slab)
-    spec.data.view(16, 16, 9)[5, 2, 8] += 1j  # a Nyquist bin of plane 5 becomes non-real
+    spec.data.view(16, 16, 9)[5, 2, 8] += 1j  # one Nyquist bin becomes non-real
     tf.inverse(fp, spec)  # no exception at the call
     tf.inverse(fp, tf.forward(fp, slab))
-    with pytest.raises(tf.ConsistencyError, match="plane 5"):
+    with pytest.raises(tf.ConsistencyError, match=r"in 2 inverse call\(s\)"):
         fp.collect_consistency()
     tf.inverse(fp, tf.forward(fp, slab))  # the accumulator was reset by the collect
     assert fp.collect_consistency() == 1
