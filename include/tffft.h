@@ -79,7 +79,10 @@ int tffft_comm_init_all(int p, const int* devices, tffft_comm_t* comms);
  * a device pull from the peers' staging (or, with TFFFT_FLAG_PEER_STORES, the
  * producing stage's stores into the peers' landing buffers), ordered by IPC
  * events; `barrier` is the only host-side collective (MPI, a gloo group, ...).
- * Ranks may share a device (several processes on one GPU) or not (P2P). */
+ * Ranks may share a device (several processes on one GPU) or not (P2P).
+ * Destroy IPC plans after a host barrier: a peer may still be enqueueing work
+ * that references this plan's exported buffers or events until it passes
+ * the barrier that ends its last exchange. */
 int tffft_comm_init_ipc(int p, int rank, int device, tffft_barrier_fn barrier, void* ctx, tffft_comm_t* comm);
 /* host barrier of a local-fabric or IPC communicator (TFFFT_ERR_CONFIGURATION on NCCL) */
 int tffft_comm_barrier(tffft_comm_t comm);
