@@ -8,6 +8,7 @@
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
 #include "col_tma.cuh"
+#include "col_wpc.cuh"
 
 namespace tffft {
 
@@ -355,6 +356,32 @@ int col_tma_width<TFFFT_REAL>(int L, bool wide) {
     case 10: return w ? (TmaColCfg<TFFFT_REAL, 10, W10>::OK ? W10 : 0) : (TmaColCfg<TFFFT_REAL, 10, N10>::OK ? N10 : 0);
     default: return 0;
   }
+}
+
+template <typename T, int L, bool INV>
+static cudaError_t wpc_one(const CUtensorMap& map, const WpcParams& p, cudaStream_t s) {
+  using WC = WpcCfg<T, L>;
+  auto k = col_wpc_kernel<T, L, INV>;
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, WC::SMEM);
+  if (prep != cudaSuccess) return prep;
+  if (p.ntiles <= 0) return cudaSuccess;
+  // persistent: one CTA per SM
+  const long long blocks = std::min<long long>(p.ntiles, (long long)num_sms());
+  (void)cudaGetLastError();
+  k<<<(unsigned)blocks, WC::THREADS, WC::SMEM, s>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const CUtensorMap& map, const WpcParams& p, cudaStream_t s) {
+  if (L != 10) return cudaErrorInvalidValue;
+  return inv ? wpc_one<TFFFT_REAL, 10, true>(map, p, s) : wpc_one<TFFFT_REAL, 10, false>(map, p, s);
+}
+
+template <>
+int col_wpc_width<TFFFT_REAL>(int L) {
+  return L == 10 && WpcCfg<TFFFT_REAL, 10>::OK ? WpcCfg<TFFFT_REAL, 10>::B : 0;
 }
 
 template <>

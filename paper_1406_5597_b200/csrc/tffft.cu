@@ -31,6 +31,7 @@
 #include "stage1_fused.cuh"
 #include "fourstep_tma.cuh"
 #include "col_tma.cuh"
+#include "col_wpc.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 #include <nvtx3/nvToolsExt.h>
@@ -470,6 +471,16 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 // ---------------------------------------------------------------------------
 // stage launchers
 // ---------------------------------------------------------------------------
+// Warp-per-column kernel (col_wpc.cuh) for the 1024-point column passes at p = 1.
+// TFFFT_WPC: 0 never, 1 every pass, 2 (default) the stage-1b / 1b' passes only.
+// Measured on one box (profiles/r02/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
+// float64 1024^3 launch; stage 3 (rows 8.4 MB apart) ties at 2.99-3.00 ms in
+// isolation and is slightly slower live, so it keeps col_tma_kernel.
+static int wpc_cols_mode() {
+  const char* e = getenv("TFFFT_WPC");
+  return e ? atoi(e) : 2;
+}
+
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
@@ -573,13 +584,14 @@ static EncodeTiledFn encode_tiled() {
 // rank-r map over `base` in real elements of the plan's precision; dims/strides innermost first
 static int make_map(tffft_plan_t pl, CUtensorMap* m, void* base, int rank, const cuuint64_t* dims,
                     const cuuint64_t* strides_bytes, const cuuint32_t* box,
-                    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+                    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = fn(m, pl->dtype == TFFFT_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         (cuuint32_t)rank, base, dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                        swz, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TFFFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return TFFFT_OK;
@@ -613,6 +625,31 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   CUtensorMap map, map_odd;
   const long long n = 1LL << L;
   const long long gbytes = ngrp > 1 ? gstride * esz : n * rbytes;
+  // warp-per-column kernel (col_wpc.cuh): 1024-point columns with 16-byte-aligned rows
+  if (!parity && (wpc_cols_mode() == 1 || (wpc_cols_mode() == 2 && !wide)) && col_wpc_supported(L)) {
+    const long long BW = pl->dtype == TFFFT_F64 ? col_wpc_width<double>(L) : col_wpc_width<float>(L);
+    if (BW > 0) {
+      cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
+      cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
+      cuuint32_t box[3] = {(cuuint32_t)(2 * BW), 256, 1};
+      TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_SWIZZLE_128B));
+      WpcParams w{};
+      w.tw = tw;
+      w.tpg = (int)((cols + BW - 1) / BW);
+      w.ntiles = (long long)w.tpg * ngrp;
+      static const char* ef = getenv("TFFFT_TMA_EF");
+      w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
+      if (TFFFT_COL_TICKET && L >= ticket_min_log(true)) {
+        w.ticket = pl->col_ticket;
+        CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
+      }
+      pl->launches++;
+      CUDA_TRY(pl->dtype == TFFFT_F64 ? launch_col_wpc<double>(L, inv, map, w, s)
+                                      : launch_col_wpc<float>(L, inv, map, w, s));
+      *done = true;
+      return TFFFT_OK;
+    }
+  }
   if (!parity) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
     cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
