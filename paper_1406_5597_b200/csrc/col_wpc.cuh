@@ -1,5 +1,6 @@
-// Warp-per-column, warp-specialised column c2c for sm_100a (1024-point columns,
-// p = 1: stages 1b / 1b' / 3 / 3').
+// Warp-per-column, warp-specialised column c2c for sm_100a (1024-point columns:
+// stages 1b / 1b' / 3 / 3' at p = 1, and the two-level stage-1b / 1b' passes at
+// p > 1 -- band-redirected stores, landing-band loads).
 //
 // col_tma_kernel (col_tma.cuh) spreads every column over all warps of the CTA
 // (thread = 4 rows x 8 columns slices), so the operand read, both FFT passes,
@@ -32,6 +33,12 @@
 //   full[q]  / empty[q]   landing box q: TMA bytes landed / all warps read it
 //   xdrained              every warp finished its exchange (stage may be written)
 //   ofull[s] / oempty[s]  output quarter slot s written / read out by the TMA store
+// p > 1: only the producer changes.  Loads may go through a 4D map over the
+// landing bands (cols, rows within a block, block, group) in sub-boxes that
+// never cross a block; stores may go through one map per destination block
+// (the forward band redirects: self band to landing[rank], peer bands to
+// staging or straight into the peer's landing buffer) -- the reference's
+// strided exchange datatype (exchange.py:114-121) applied by the TMA boxes.
 // Same engine, twiddles and arithmetic as col_tma_kernel: results are bitwise
 // identical (tests/test_gpu_parity.py::test_wpc_column_kernel_bitwise).
 //
@@ -72,17 +79,31 @@ struct WpcCfg {
                              E % NBOX == 0 && SH::RL == E && SH::R0 == E;
 };
 
+constexpr int kWpcMaps = 16;  // store maps (destination blocks, p <= 16)
+
 struct WpcParams {
   const void* tw;              // pass tables (fft_engine.cuh layout)
   long long ntiles;
   int tpg;                     // tiles per group
   int evict_first;             // L2 priority of the loads and stores
   unsigned long long* ticket;  // dynamic tile order (zeroed before the launch), or null: round robin
+  int load4;                   // 4D load map (2*cols, rows_in, blocks, groups): row r at (r mod rows_in, r >> lin_shift)
+  int lin_shift;               // log2(rows_in)
+  int lbrows;                  // rows per load sub-box (divides 256, multiple of 8, <= rows_in)
+  int nst;                     // store maps: 1 = uniform (row r of the column at row r of st[0])
+  int sst_shift;               // nst > 1: log2(rows per destination block); row r -> st[r >> sst_shift]
+  int sbrows;                  // rows per store sub-box (divides 256, multiple of 8, <= rows per block)
+};
+
+// tensor maps of one launch: every box is B columns x (sub-box rows), 128-byte swizzle
+struct alignas(64) WpcMaps {
+  CUtensorMap ld;
+  CUtensorMap st[kWpcMaps];
 };
 
 template <typename T, int L, bool INV>
 __global__ void __launch_bounds__(WpcCfg<T, L>::THREADS, 1)
-col_wpc_kernel(const __grid_constant__ CUtensorMap map, const WpcParams prm) {
+col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   using WC = WpcCfg<T, L>;
   using SH = Shape<L>;
   using ST = Stockham<T, L, INV, WC::S, WC::PS, true, 32, true>;
@@ -133,7 +154,15 @@ col_wpc_kernel(const __grid_constant__ CUtensorMap map, const WpcParams prm) {
       const int grp = (int)(tile / prm.tpg), c0 = (int)(tile % prm.tpg) * B;
       fence_async_shared();
       mbar_arrive_tx(full + q, (unsigned)WC::BOXB);
-      tma_load3(ring + (size_t)q * WC::BOXB, &map, 2 * c0, q * BOX, grp, full + q, pol);
+      unsigned char* dst = ring + (size_t)q * WC::BOXB;
+      if (prm.load4) {  // two-level rows: sub-boxes never cross a block
+        const int rmask = (1 << prm.lin_shift) - 1;
+        for (int r = q * BOX; r < (q + 1) * BOX; r += prm.lbrows)
+          tma_load4(dst + (size_t)(r - q * BOX) * 128, &maps.ld, 2 * c0, r & rmask, r >> prm.lin_shift, grp, full + q,
+                    pol);
+      } else {
+        tma_load3(dst, &maps.ld, 2 * c0, q * BOX, grp, full + q, pol);
+      }
     };
     // the output stage starts empty
     mbar_arrive(oempty + 0);
@@ -161,7 +190,14 @@ col_wpc_kernel(const __grid_constant__ CUtensorMap map, const WpcParams prm) {
       for (int qq = 0; qq < NBOX; ++qq) {
         const int s = qq & 1;
         mbar_wait(ofull + s, (unsigned)(((it * (NBOX / 2)) + (qq >> 1)) & 1u));
-        tma_store3(&map, 2 * c0, qq * BOX, grp, xs + (size_t)s * WC::BOXB, pol);
+        const unsigned char* src = xs + (size_t)s * WC::BOXB;
+        if (prm.nst > 1) {  // block redirect: row r goes to row (r mod block rows) of st[r / block rows]
+          const int smask = (1 << prm.sst_shift) - 1;
+          for (int r = qq * BOX; r < (qq + 1) * BOX; r += prm.sbrows)
+            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - qq * BOX) * 128, pol);
+        } else {
+          tma_store3(&maps.st[0], 2 * c0, qq * BOX, grp, src, pol);
+        }
         bulk_commit();
         if (s == 1) {
           bulk_wait_read1();  // slot 0 has been read out
@@ -231,7 +267,7 @@ col_wpc_kernel(const __grid_constant__ CUtensorMap map, const WpcParams prm) {
 __host__ __device__ constexpr bool col_wpc_supported(int L) { return L == 10; }
 
 template <typename T>
-cudaError_t launch_col_wpc(int L, bool inv, const CUtensorMap& map, const WpcParams& p, cudaStream_t s);
+cudaError_t launch_col_wpc(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s);
 // columns per tile (the box width; 0: no kernel for this length)
 template <typename T>
 int col_wpc_width(int L);

@@ -359,7 +359,7 @@ int col_tma_width<TFFFT_REAL>(int L, bool wide) {
 }
 
 template <typename T, int L, bool INV>
-static cudaError_t wpc_one(const CUtensorMap& map, const WpcParams& p, cudaStream_t s) {
+static cudaError_t wpc_one(const WpcMaps& maps, const WpcParams& p, cudaStream_t s) {
   using WC = WpcCfg<T, L>;
   auto k = col_wpc_kernel<T, L, INV>;
   static KernelCache kc;
@@ -369,14 +369,14 @@ static cudaError_t wpc_one(const CUtensorMap& map, const WpcParams& p, cudaStrea
   // persistent: one CTA per SM
   const long long blocks = std::min<long long>(p.ntiles, (long long)num_sms());
   (void)cudaGetLastError();
-  k<<<(unsigned)blocks, WC::THREADS, WC::SMEM, s>>>(map, p);
+  k<<<(unsigned)blocks, WC::THREADS, WC::SMEM, s>>>(maps, p);
   return cudaGetLastError();
 }
 
 template <>
-cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const CUtensorMap& map, const WpcParams& p, cudaStream_t s) {
+cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s) {
   if (L != 10) return cudaErrorInvalidValue;
-  return inv ? wpc_one<TFFFT_REAL, 10, true>(map, p, s) : wpc_one<TFFFT_REAL, 10, false>(map, p, s);
+  return inv ? wpc_one<TFFFT_REAL, 10, true>(maps, p, s) : wpc_one<TFFFT_REAL, 10, false>(maps, p, s);
 }
 
 template <>

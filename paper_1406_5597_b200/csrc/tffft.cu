@@ -471,16 +471,6 @@ __global__ void permute_rows_kernel(const PermuteParams p, int esz) {
 // ---------------------------------------------------------------------------
 // stage launchers
 // ---------------------------------------------------------------------------
-// Warp-per-column kernel (col_wpc.cuh) for the 1024-point column passes at p = 1.
-// TFFFT_WPC: 0 never, 1 every pass, 2 (default) the stage-1b / 1b' passes only.
-// Measured on one box (profiles/r02/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
-// float64 1024^3 launch; stage 3 (rows 8.4 MB apart) ties at 2.99-3.00 ms in
-// isolation and is slightly slower live, so it keeps col_tma_kernel.
-static int wpc_cols_mode() {
-  const char* e = getenv("TFFFT_WPC");
-  return e ? atoi(e) : 2;
-}
-
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done);
 
@@ -609,6 +599,91 @@ static bool tma_cols_enabled(tffft_plan_t pl, int L) {
   return pl->tma_cols != 0;
 }
 
+// Warp-per-column kernel (col_wpc.cuh) for the 1024-point column passes at p = 1.
+// TFFFT_WPC: 0 never, 1 every pass, 2 (default) the stage-1b / 1b' passes only.
+// Measured on one box (profiles/r02/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
+// float64 1024^3 launch; stage 3 (rows 8.4 MB apart) ties at 2.99-3.00 ms in
+// isolation and is slightly slower live, so it keeps col_tma_kernel.
+static int wpc_cols_mode() {
+  const char* e = getenv("TFFFT_WPC");
+  return e ? atoi(e) : 2;
+}
+
+// Column pass through the warp-per-column kernel: loads as columns_tma_two
+// describes them (3D map, or 4D over the landing bands), stores uniform
+// (st_tab empty: row r of the column at st_base + r * st_in) or one map per
+// destination block (st_tab[r / st_rows], row r mod st_rows).  *done = false
+// when the mode, the shape or an alignment rules it out.
+static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, const void* tw, cudaStream_t s,
+                       bool* done) {
+  *done = false;
+  const int mode = wpc_cols_mode();
+  if (!(mode == 1 || (mode == 2 && !j.wide)) || !col_wpc_supported(L)) return TFFFT_OK;
+  const long long esz = (long long)pl->esz, n = 1LL << L;
+  const long long B = pl->dtype == TFFFT_F64 ? col_wpc_width<double>(L) : col_wpc_width<float>(L);
+  const bool two = !j.st_tab.empty();
+  if (B <= 0 || j.ld_in_rows * j.ld_blocks != n || (int)j.st_tab.size() > kWpcMaps) return TFFFT_OK;
+  if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
+      reinterpret_cast<uintptr_t>(j.ld_base) % 16 || (j.st_in * esz) % 16 || (j.ngrp > 1 && (j.st_g * esz) % 16))
+    return TFFFT_OK;
+  const long long lbrows = std::min<long long>(256, j.ld_in_rows);
+  const long long srows_blk = two ? j.st_rows : n, sbrows = std::min<long long>(256, srows_blk);
+  // sub-boxes start on 1024-byte (8-row) boundaries of the swizzled landing boxes
+  if (lbrows < 8 || sbrows < 8 || (two && srows_blk * (long long)j.st_tab.size() != n)) return TFFFT_OK;
+  for (void* d : j.st_tab)
+    if (reinterpret_cast<uintptr_t>(d) % 16) return TFFFT_OK;
+  if (!two && reinterpret_cast<uintptr_t>(j.st_base) % 16) return TFFFT_OK;
+  WpcMaps maps;
+  if (j.ld_blocks == 1) {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)n, (cuuint64_t)j.ngrp};
+    cuuint64_t st[2] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * B), 256, 1};
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B));
+  } else {
+    cuuint64_t d[4] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)j.ld_in_rows, (cuuint64_t)j.ld_blocks,
+                       (cuuint64_t)j.ngrp};
+    cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
+                        (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * B), (cuuint32_t)lbrows, 1, 1};
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  const int nst = two ? (int)j.st_tab.size() : 1;
+  for (int q = 0; q < nst; ++q) {
+    cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)srows_blk, (cuuint64_t)j.ngrp};
+    cuuint64_t st[2] = {(cuuint64_t)(j.st_in * esz),
+                        (cuuint64_t)(j.ngrp > 1 ? j.st_g * esz : srows_blk * j.st_in * esz)};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)sbrows, 1};
+    TRY(make_map(pl, &maps.st[q], two ? j.st_tab[q] : j.st_base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  for (int q = nst; q < kWpcMaps; ++q) maps.st[q] = maps.st[0];
+  WpcParams w{};
+  w.tw = tw;
+  w.tpg = (int)((j.cols + B - 1) / B);
+  w.ntiles = (long long)w.tpg * j.ngrp;
+  {
+    static const char* ef = getenv("TFFFT_TMA_EF");
+    w.evict_first = ef ? atoi(ef) : ((j.ld_in * esz) % 128 == 0);
+  }
+  w.load4 = j.ld_blocks > 1;
+  w.lin_shift = ilog2(j.ld_in_rows);
+  w.lbrows = (int)lbrows;
+  w.nst = nst;
+  w.sst_shift = ilog2(srows_blk);
+  w.sbrows = (int)sbrows;
+  if (TFFFT_COL_TICKET && L >= ticket_min_log(true)) {
+    w.ticket = pl->col_ticket;
+    CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
+  }
+  pl->launches++;
+  CUDA_TRY(pl->dtype == TFFFT_F64 ? launch_col_wpc<double>(L, inv, maps, w, s)
+                                  : launch_col_wpc<float>(L, inv, maps, w, s));
+  *done = true;
+  return TFFFT_OK;
+}
+
 static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, long long cols, long long ngrp,
                        long long rstride, long long gstride, const void* tw, cudaStream_t s, bool* done) {
   *done = false;
@@ -625,30 +700,14 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   CUtensorMap map, map_odd;
   const long long n = 1LL << L;
   const long long gbytes = ngrp > 1 ? gstride * esz : n * rbytes;
-  // warp-per-column kernel (col_wpc.cuh): 1024-point columns with 16-byte-aligned rows
-  if (!parity && (wpc_cols_mode() == 1 || (wpc_cols_mode() == 2 && !wide)) && col_wpc_supported(L)) {
-    const long long BW = pl->dtype == TFFFT_F64 ? col_wpc_width<double>(L) : col_wpc_width<float>(L);
-    if (BW > 0) {
-      cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
-      cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
-      cuuint32_t box[3] = {(cuuint32_t)(2 * BW), 256, 1};
-      TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_SWIZZLE_128B));
-      WpcParams w{};
-      w.tw = tw;
-      w.tpg = (int)((cols + BW - 1) / BW);
-      w.ntiles = (long long)w.tpg * ngrp;
-      static const char* ef = getenv("TFFFT_TMA_EF");
-      w.evict_first = ef ? atoi(ef) : (rbytes % 128 == 0);
-      if (TFFFT_COL_TICKET && L >= ticket_min_log(true)) {
-        w.ticket = pl->col_ticket;
-        CUDA_TRY(cudaMemsetAsync(pl->col_ticket, 0, sizeof(unsigned long long), s));
-      }
-      pl->launches++;
-      CUDA_TRY(pl->dtype == TFFFT_F64 ? launch_col_wpc<double>(L, inv, map, w, s)
-                                      : launch_col_wpc<float>(L, inv, map, w, s));
-      *done = true;
-      return TFFFT_OK;
-    }
+  if (!parity) {  // warp-per-column kernel (col_wpc.cuh) where it applies
+    TwoLevelJob j{};
+    j.wide = wide;
+    j.ld_base = base; j.cols = cols; j.ngrp = ngrp;
+    j.ld_in_rows = n; j.ld_blocks = 1; j.ld_in = rstride; j.ld_out = 0; j.ld_g = gstride;
+    j.st_base = base; j.st_rows = n; j.st_in = rstride; j.st_g = gstride;
+    TRY(columns_wpc(pl, L, inv, j, tw, s, done));
+    if (*done) return TFFFT_OK;
   }
   if (!parity) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
@@ -714,7 +773,10 @@ static int columns_tma_two(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& 
   *done = false;
   const long long esz = (long long)pl->esz, n = 1LL << L;
   const bool two = !j.st_tab.empty();
-  if (!tma_cols_enabled(pl, L) || !col_tma_supported(L) || (int)j.st_tab.size() > kTmaTab) return TFFFT_OK;
+  if (!tma_cols_enabled(pl, L)) return TFFFT_OK;
+  TRY(columns_wpc(pl, L, inv, j, tw, s, done));
+  if (*done) return TFFFT_OK;
+  if (!col_tma_supported(L) || (int)j.st_tab.size() > kTmaTab) return TFFFT_OK;
   if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
       reinterpret_cast<uintptr_t>(j.ld_base) % 16)
     return TFFFT_OK;

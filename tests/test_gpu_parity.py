@@ -425,6 +425,54 @@ def test_tma_column_kernel_bitwise(shape, p, dtype):
         assert rel(back, x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
 
 
+WPC_CASES = [((1024, 16, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((16, 1024, 64), 1),
+             ((32, 1024, 16), 2), ((32, 1024, 16), 4), ((64, 1024, 16), 8), ((16, 1024, 8), 16)]
+
+
+@pytest.mark.parametrize("shape,p", WPC_CASES, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_wpc_column_kernel_bitwise(shape, p, dtype, monkeypatch):
+    """Warp-per-column kernel (col_wpc.cuh, 1024-point columns): one warp owns
+    a column, operands from the swizzled TMA landing ring, outputs through TMA
+    stores.  Same engine and twiddles as col_tma_kernel, so with it on every
+    1024-point pass (TFFFT_WPC=1), on the stage-1b passes only (the default,
+    2) or off (0) the spectra and inverse outputs are bitwise identical, and
+    within tolerance of the oracle.  Covers partial tiles (n2c = 5, 9, 33
+    columns per group), more CTAs than tiles, the float32 stage-1b rows that
+    miss 16-byte alignment (fall back to col_tma_kernel), and p > 1: forward
+    stage 1b storing every band through its own tensor map (band redirects),
+    inverse stage 1b' loading the landing bands through the 4D map, with
+    blocks of 512 down to 64 rows."""
+    x = oracle.uniform_field(shape, seed=37)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        fp = tf.plan(grid, ep, dtype=dtype)
+        for _ in range(2):  # twice: the ticket counter and the mbarrier phases start over per launch
+            spec = tf.forward(fp, slabs[ep.rank]).data.clone()
+            back = tf.inverse(fp, tf.SpectralSlab(fp.spectral_layout, tf.SpectralTag.STRIDED_INPLACE,
+                                                  spec.clone())).data.clone()
+        res = (spec.cpu().numpy(), back.cpu().numpy())
+        fp.close()
+        return res
+
+    out = {}
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("TFFFT_WPC", mode)
+        out[mode] = tf.run_spmd(p, body)
+    ref = oracle.forward_all(x, p)
+    n0p = shape[0] // p
+    for q in range(p):
+        for mode in ("1", "2"):
+            assert np.array_equal(out[mode][q][0], out["0"][q][0])
+            assert np.array_equal(out[mode][q][1], out["0"][q][1])
+        assert rel(out["2"][q][0], ref[q]) <= TOL[dtype]
+        assert rel(out["2"][q][1], x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
+
+
 @pytest.mark.parametrize("p", [1, 2, 4])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_constant_and_delta_known_answers(p, dtype):

@@ -35,6 +35,10 @@ CASES = [
     ((64, 64, 32), 4, {"batch": 3}),                                     # batched pipeline, 2 buffer sets
     ((512, 32, 16), 2, {"batch": 4, "algorithms": ("peer_stores", "tma_columns")}),
     ((1024, 32, 16), 4, {"algorithms": ("chunked_exchange", "tma_columns")}),      # plane-chunked forward
+    ((16, 1024, 32), 1, {}),                                             # warp-per-column stage 1b, p = 1
+    ((32, 1024, 16), 4, {}),                                             # warp-per-column two-level stage 1b
+    ((32, 1024, 16), 8, {"algorithms": ("peer_stores", "tma_columns")}),  # ... storing into the peers' landing
+    ((32, 1024, 16), 2, {"batch": 3}),                                   # ... in the batched pipeline
 ]
 
 
