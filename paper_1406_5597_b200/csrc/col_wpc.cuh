@@ -83,6 +83,7 @@ constexpr int kWpcMaps = 16;  // store maps (destination blocks, p <= 16)
 
 struct WpcParams {
   const void* tw;              // pass tables (fft_engine.cuh layout)
+  const void* tw2;             // 2 x 1024 kernel (col_wpc2.cuh): exp(-2 pi i k / 2048), k < 1024
   long long ntiles;
   int tpg;                     // tiles per group
   int evict_first;             // L2 priority of the loads and stores
@@ -263,8 +264,8 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   }
 }
 
-// 1024-point columns only
-__host__ __device__ constexpr bool col_wpc_supported(int L) { return L == 10; }
+// 1024-point columns; 2048-point columns as 2 x 1024 (col_wpc2.cuh)
+__host__ __device__ constexpr bool col_wpc_supported(int L) { return L == 10 || L == 11; }
 
 template <typename T>
 cudaError_t launch_col_wpc(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s);

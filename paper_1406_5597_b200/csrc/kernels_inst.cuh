@@ -9,6 +9,7 @@
 #include "fourstep_tma.cuh"
 #include "col_tma.cuh"
 #include "col_wpc.cuh"
+#include "col_wpc2.cuh"
 
 namespace tffft {
 
@@ -373,14 +374,31 @@ static cudaError_t wpc_one(const WpcMaps& maps, const WpcParams& p, cudaStream_t
   return cudaGetLastError();
 }
 
+template <typename T, bool INV>
+static cudaError_t wpc2_one(const WpcMaps& maps, const WpcParams& p, cudaStream_t s) {
+  using WC = WpcCfg<T, 10>;
+  using W2 = Wpc2Cfg<T>;
+  auto k = col_wpc2_kernel<T, INV>;
+  static KernelCache kc;
+  const cudaError_t prep = prep_smem(k, kc, W2::SMEM);
+  if (prep != cudaSuccess) return prep;
+  if (p.ntiles <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>(p.ntiles, (long long)num_sms());  // one CTA per SM (all of its TMEM)
+  (void)cudaGetLastError();
+  k<<<(unsigned)blocks, WC::THREADS, W2::SMEM, s>>>(maps, p);
+  return cudaGetLastError();
+}
+
 template <>
 cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s) {
+  if (L == 11) return inv ? wpc2_one<TFFFT_REAL, true>(maps, p, s) : wpc2_one<TFFFT_REAL, false>(maps, p, s);
   if (L != 10) return cudaErrorInvalidValue;
   return inv ? wpc_one<TFFFT_REAL, 10, true>(maps, p, s) : wpc_one<TFFFT_REAL, 10, false>(maps, p, s);
 }
 
 template <>
 int col_wpc_width<TFFFT_REAL>(int L) {
+  if (L == 11) return Wpc2Cfg<TFFFT_REAL>::OK ? WpcCfg<TFFFT_REAL, 10>::B : 0;
   return L == 10 && WpcCfg<TFFFT_REAL, 10>::OK ? WpcCfg<TFFFT_REAL, 10>::B : 0;
 }
 

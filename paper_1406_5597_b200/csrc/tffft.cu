@@ -32,6 +32,7 @@
 #include "fourstep_tma.cuh"
 #include "col_tma.cuh"
 #include "col_wpc.cuh"
+#include "col_wpc2.cuh"
 #include "kernels.cuh"
 #include "nccl.h"
 #include <nvtx3/nvToolsExt.h>
@@ -293,6 +294,8 @@ struct tffft_plan_s {
   void* tw2r = nullptr;  // row pass tables in the r2c kernel's schedule
   void* tw2c = nullptr;  // row pass tables in the c2r kernel's schedule
   void* tw2post = nullptr;
+  void* tw10 = nullptr;    // 2 x 1024 column kernel (col_wpc2.cuh): the 1024-point pass tables ...
+  void* twh11 = nullptr;   // ... and exp(-2 pi i k / 2048), k < 1024
   unsigned long long* stats = nullptr;  // per plane [m2, edge, residue] (ordered doubles), batch * n0p planes
   double* row_stats = nullptr;          // per row records of the c2r kernel
   // stage-3 four-step (fourstep.cuh): L2-resident scratch ring, counters, tables
@@ -600,7 +603,11 @@ static bool tma_cols_enabled(tffft_plan_t pl, int L) {
 }
 
 // Warp-per-column kernel (col_wpc.cuh) for the 1024-point column passes at p = 1.
-// TFFFT_WPC: 0 never, 1 every pass, 2 (default) the stage-1b / 1b' passes only.
+// TFFFT_WPC: 0 never, 1 every pass, 2 (default) the stage-1b / 1b' passes, and
+// for float32 the stage-3 / 3' passes too (3.41 -> 3.28 ms per pair live).  The
+// float32 stage-1b rows of an odd n2c (8 bytes off 16-byte alignment on odd rows)
+// stay on col_tma_kernel: a swizzled box must start on a 16-byte boundary (a box
+// started one complex in raised "illegal instruction" on the B200).
 // Measured on one box (profiles/r02/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
 // float64 1024^3 launch; stage 3 (rows 8.4 MB apart) ties at 2.99-3.00 ms in
 // isolation and is slightly slower live, so it keeps col_tma_kernel.
@@ -618,7 +625,10 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
                        bool* done) {
   *done = false;
   const int mode = wpc_cols_mode();
-  if (!(mode == 1 || (mode == 2 && !j.wide)) || !col_wpc_supported(L)) return TFFFT_OK;
+  const bool x2 = L == 11;  // 2048 points as 2 x 1024 (col_wpc2.cuh): every pass, col_fft_kernel is far slower there
+  if (!(mode == 1 || (mode == 2 && (!j.wide || pl->dtype == TFFFT_F32 || x2))) || !col_wpc_supported(L))
+    return TFFFT_OK;
+  if (x2 && (!pl->tw10 || !pl->twh11 || j.ld_in_rows % 2)) return TFFFT_OK;
   const long long esz = (long long)pl->esz, n = 1LL << L;
   const long long B = pl->dtype == TFFFT_F64 ? col_wpc_width<double>(L) : col_wpc_width<float>(L);
   const bool two = !j.st_tab.empty();
@@ -626,7 +636,8 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
   if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
       reinterpret_cast<uintptr_t>(j.ld_base) % 16 || (j.st_in * esz) % 16 || (j.ngrp > 1 && (j.st_g * esz) % 16))
     return TFFFT_OK;
-  const long long lbrows = std::min<long long>(256, j.ld_in_rows);
+  // 2 x 1024: loads by row parity, sub-boxes of half rows within a block
+  const long long lbrows = std::min<long long>(256, x2 ? j.ld_in_rows / 2 : j.ld_in_rows);
   const long long srows_blk = two ? j.st_rows : n, sbrows = std::min<long long>(256, srows_blk);
   // sub-boxes start on 1024-byte (8-row) boundaries of the swizzled landing boxes
   if (lbrows < 8 || sbrows < 8 || (two && srows_blk * (long long)j.st_tab.size() != n)) return TFFFT_OK;
@@ -634,7 +645,22 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     if (reinterpret_cast<uintptr_t>(d) % 16) return TFFFT_OK;
   if (!two && reinterpret_cast<uintptr_t>(j.st_base) % 16) return TFFFT_OK;
   WpcMaps maps;
-  if (j.ld_blocks == 1) {
+  if (x2 && j.ld_blocks == 1) {  // (cols, parity, half rows, groups)
+    cuuint64_t d[4] = {(cuuint64_t)(2 * j.cols), 2, (cuuint64_t)(n / 2), (cuuint64_t)j.ngrp};
+    cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz),
+                        (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * B), 1, 256, 1};
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B));
+  } else if (x2) {  // (cols, parity, half rows within a block, blocks, groups)
+    cuuint64_t d[5] = {(cuuint64_t)(2 * j.cols), 2, (cuuint64_t)(j.ld_in_rows / 2), (cuuint64_t)j.ld_blocks,
+                       (cuuint64_t)j.ngrp};
+    cuuint64_t st[4] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
+                        (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
+    cuuint32_t box[5] = {(cuuint32_t)(2 * B), 1, (cuuint32_t)lbrows, 1, 1};
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 5, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B));
+  } else if (j.ld_blocks == 1) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)n, (cuuint64_t)j.ngrp};
     cuuint64_t st[2] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
     cuuint32_t box[3] = {(cuuint32_t)(2 * B), 256, 1};
@@ -660,7 +686,8 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
   }
   for (int q = nst; q < kWpcMaps; ++q) maps.st[q] = maps.st[0];
   WpcParams w{};
-  w.tw = tw;
+  w.tw = x2 ? pl->tw10 : tw;
+  w.tw2 = pl->twh11;
   w.tpg = (int)((j.cols + B - 1) / B);
   w.ntiles = (long long)w.tpg * j.ngrp;
   {
@@ -692,15 +719,9 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
   // rows 16-byte aligned (one map), or 8 bytes off on odd rows only (float32
   // stage 1b, n2c odd: 4104-byte rows): even and odd rows through two maps
   const bool parity = rbytes % 16 != 0;
-  if (!tma_cols_enabled(pl, L) || !col_tma_supported(L) || (parity && (2 * rbytes) % 16) ||
-      (ngrp > 1 && (gstride * esz) % 16) || reinterpret_cast<uintptr_t>(base) % 16)
-    return TFFFT_OK;
-  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
-  if (B <= 0) return TFFFT_OK;
-  CUtensorMap map, map_odd;
+  if (!tma_cols_enabled(pl, L)) return TFFFT_OK;
   const long long n = 1LL << L;
-  const long long gbytes = ngrp > 1 ? gstride * esz : n * rbytes;
-  if (!parity) {  // warp-per-column kernel (col_wpc.cuh) where it applies
+  if (!parity) {  // warp-per-column kernel (col_wpc.cuh, col_wpc2.cuh) where it applies
     TwoLevelJob j{};
     j.wide = wide;
     j.ld_base = base; j.cols = cols; j.ngrp = ngrp;
@@ -709,6 +730,13 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
     TRY(columns_wpc(pl, L, inv, j, tw, s, done));
     if (*done) return TFFFT_OK;
   }
+  if (!col_tma_supported(L) || (parity && (2 * rbytes) % 16) || (ngrp > 1 && (gstride * esz) % 16) ||
+      reinterpret_cast<uintptr_t>(base) % 16)
+    return TFFFT_OK;
+  const long long B = pl->dtype == TFFFT_F64 ? col_tma_width<double>(L, wide) : col_tma_width<float>(L, wide);
+  if (B <= 0) return TFFFT_OK;
+  CUtensorMap map, map_odd;
+  const long long gbytes = ngrp > 1 ? gstride * esz : n * rbytes;
   if (!parity) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
     cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
@@ -1684,6 +1712,10 @@ int tffft_plan_create_batched(int n0, int n1, int n2, int dtype, int pattern, in
   TRY(upload_table(pass_table(pl->L2h, r2c_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2r, &ws));
   TRY(upload_table(pass_table(pl->L2h, c2r_radix_bits(pl->L2h, pl->esz / 2)), dtype, &pl->tw2c, &ws));
   TRY(upload_table(post_table(n2), dtype, &pl->tw2post, &ws));
+  if (pl->L0 == 11 || pl->L1 == 11) {
+    TRY(upload_table(pass_table(10), dtype, &pl->tw10, &ws));
+    TRY(upload_table(post_table(2048), dtype, &pl->twh11, &ws));
+  }
   CUDA_TRY(cudaMalloc(&pl->col_ticket, sizeof(unsigned long long)));
   const size_t planes = (size_t)batch * pl->n0p;  // statistics records: every plane of the batch
   CUDA_TRY(cudaMalloc(&pl->stats, sizeof(unsigned long long) * 3 * planes));
@@ -1837,7 +1869,7 @@ int tffft_plan_destroy(tffft_plan_t pl) {
   cudaSetDevice(pl->comm->device);
   if (pl->xstream) cudaStreamSynchronize(pl->xstream);
   free_events(pl);
-  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2c); cudaFree(pl->tw2post);
+  cudaFree(pl->tw0); cudaFree(pl->tw1); cudaFree(pl->tw2); cudaFree(pl->tw2r); cudaFree(pl->tw2c); cudaFree(pl->tw2post); cudaFree(pl->tw10); cudaFree(pl->twh11);
   cudaFree(pl->stats); cudaFree(pl->row_stats);
   for (void* m : pl->ipc_opened) cudaIpcCloseMemHandle(m);
   for (cudaEvent_t e : pl->ipc_events) cudaEventDestroy(e);

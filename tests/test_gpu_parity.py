@@ -473,6 +473,49 @@ def test_wpc_column_kernel_bitwise(shape, p, dtype, monkeypatch):
         assert rel(out["2"][q][1], x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
 
 
+WPC2_CASES = [((2048, 16, 8), 1), ((8, 2048, 16), 1), ((2048, 2048, 4), 1), ((16, 2048, 64), 1),
+              ((2048, 32, 16), 2), ((32, 2048, 16), 4), ((2048, 2048, 2), 8), ((64, 2048, 8), 16),
+              ((2048, 64, 4), 64)]
+
+
+@pytest.mark.parametrize("shape,p", WPC2_CASES, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_wpc2_2048_point_columns_vs_oracle(shape, p, dtype, monkeypatch):
+    """2048-point columns as 2 x 1024 on the warp-per-column kernel with the
+    even half parked in tensor memory (col_wpc2.cuh): stage 1b / 1b' (n1 =
+    2048) and stage 3 / 3' (n0 = 2048), p = 1 and the two-level variants
+    (row-parity 5D landing loads, one store map per destination block) down
+    to blocks of 32 rows (p = 64: 16 half rows per sub-box).  Against the
+    oracle, and against col_fft_kernel (TFFFT_WPC=0) within the same
+    tolerance (a different factorisation: not bitwise)."""
+    x = oracle.uniform_field(shape, seed=41)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p, dtype=dtype)
+
+    def body(ep):
+        fp = tf.plan(grid, ep, dtype=dtype)
+        for _ in range(2):
+            spec = tf.forward(fp, slabs[ep.rank]).data.clone()
+            back = tf.inverse(fp, tf.SpectralSlab(fp.spectral_layout, tf.SpectralTag.STRIDED_INPLACE,
+                                                  spec.clone())).data.clone()
+        res = (spec.cpu().numpy(), back.cpu().numpy())
+        fp.close()
+        return res
+
+    out = {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("TFFFT_WPC", mode)
+        out[mode] = tf.run_spmd(p, body)
+    ref = oracle.forward_all(x, p)
+    n0p = shape[0] // p
+    for q in range(p):
+        assert rel(out["2"][q][0], ref[q]) <= TOL[dtype]
+        assert rel(out["2"][q][1], x[q * n0p:(q + 1) * n0p].reshape(-1)) <= TOL[dtype]
+        assert rel(out["2"][q][0], out["0"][q][0]) <= TOL[dtype]
+
+
 @pytest.mark.parametrize("p", [1, 2, 4])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_constant_and_delta_known_answers(p, dtype):

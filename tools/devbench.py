@@ -13,13 +13,15 @@ ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--dtype", default="float64")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--check", action="store_true")
+ap.add_argument("--shape", default=None, help="n0,n1,n2 (overrides --n)")
 a = ap.parse_args()
 n = a.n
-grid = tf.GlobalGrid(n, n, n)
+n0, n1, n2 = (int(v) for v in a.shape.split(",")) if a.shape else (n, n, n)
+grid = tf.GlobalGrid(n0, n1, n2)
 ep = tf.make_communicators(1)[0]
 fp = tf.plan(grid, ep, check_consistency=False, dtype=a.dtype)
 rdt = tf.DTYPES[a.dtype][1]
-x = (torch.rand(n * n * n, dtype=torch.float64, device="cuda") * 2 - 1).to(rdt)
+x = (torch.rand(n0 * n1 * n2, dtype=torch.float64, device="cuda") * 2 - 1).to(rdt)
 slab = tf.RealSlab(fp.real_layout, x)
 for _ in range(int(os.environ.get("WARM", "2"))):
     tf.inverse(fp, tf.forward(fp, slab))
@@ -33,18 +35,18 @@ for _ in range(a.iters):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
-N = n ** 3
+N = n0 * n1 * n2
 import math
 gflops = 5 * N * math.log2(N) / (ms * 1e-3) / 1e9
 s_r = 8 if a.dtype == "float64" else 4
-hbm = 2 * (s_r * N + 3 * 2 * s_r * n * n * (n // 2 + 1))
+hbm = 2 * (s_r * N + 3 * 2 * s_r * n0 * n1 * (n2 // 2 + 1))
 t = fp.timers_us
-print(f"n={n} {a.dtype} pair {ms:.3f} ms  {gflops:.0f} GFLOP/s  roofline-HBM(6539) {hbm/6539e9*1e3:.3f} ms -> frac {hbm/6539e9*1e3/ms:.3f}")
+print(f"n={n0}x{n1}x{n2} {a.dtype} pair {ms:.3f} ms  {gflops:.0f} GFLOP/s  roofline-HBM(6539) {hbm/6539e9*1e3:.3f} ms -> frac {hbm/6539e9*1e3/ms:.3f}")
 print("per-pair stage ms:", {k: round(v / 1e3 / a.iters, 3) for k, v in t.items()})
 if a.check:
-    xr = x.double().view(n, n, n)
+    xr = x.double().view(n0, n1, n2)
     ref = torch.fft.rfftn(xr)
-    spec = tf.forward(fp, slab).data.view(n, n, n // 2 + 1).to(torch.complex128)
+    spec = tf.forward(fp, slab).data.view(n0, n1, n2 // 2 + 1).to(torch.complex128)
     err = (torch.linalg.norm(spec - ref) / torch.linalg.norm(ref)).item()
     back = tf.inverse(fp, tf.forward(fp, slab)).data.double()
     rt = (torch.linalg.norm(back - x.double()) / torch.linalg.norm(x.double())).item()
