@@ -5,7 +5,7 @@
 // register file (one warp per column holds 32 values per lane) nor shared
 // memory next to the landing ring.  col_fft_kernel therefore runs 2048-point
 // columns 4 at a time (64-byte row visits) and reaches 3.4-3.6 TB/s
-// (profiles/r02/l11_before.txt).  Here the column splits by row parity
+// (profiles/r02s4/l11_before.txt).  Here the column splits by row parity
 // (decimation in time):
 //
 //   E = FFT_1024(even rows), O = FFT_1024(odd rows),
@@ -20,7 +20,10 @@
 // idle in an FFT) and reads them back eight at a time while it combines
 // (tcgen05.ld).  TMEM here is a register-spill parking lot next to the SM, not
 // an MMA accumulator.  The 2048 output rows leave through the shared output
-// stage in eight 256-row rounds.
+// stage in sixteen 128-row rounds over four 16 KB slots; the producer releases
+// a slot two rounds after its store was issued, so no warp waits for a store
+// that has only just been committed (with two 32 KB slots the consumers spent
+// 19% of their stall samples in that rendezvous, profiles/r02s4/wpc2_2048.txt).
 //
 // Loads go through a map with the row parity as its own dimension: (cols,
 // parity, half rows, groups), or at p > 1 (cols, parity, half rows within a
@@ -134,8 +137,11 @@ struct Wpc2Cfg {
   static constexpr int TCOLS = 256;                               // TMEM columns: (consumer warps / 4) x NW
   static_assert((WC::B / 4) * NW == TCOLS, "tensor-memory columns");
   static constexpr size_t W2B = sizeof(cx<T>) * (size_t)NH;       // w^k, k < 1024
-  static constexpr size_t SMEM = WC::RING + WC::XS + sizeof(cx<T>) * WC::TW + W2B + 8 * WC::NBAR + 32;
-  static constexpr bool OK = WC::OK && SMEM <= 227 * 1024;
+  static constexpr int NSLOT = 4, OROWS = 128;                    // output stage: slots of OROWS rows
+  static constexpr size_t SLOTB = (size_t)OROWS * 128;
+  static constexpr int NBAR = 2 * WC::NBOX + 1 + 2 * NSLOT;
+  static constexpr size_t SMEM = WC::RING + WC::XS + sizeof(cx<T>) * WC::TW + W2B + 8 * NBAR + 32;
+  static constexpr bool OK = WC::OK && SMEM <= 227 * 1024 && NSLOT * SLOTB <= WC::XS;
 };
 
 template <typename T, bool INV>
@@ -145,8 +151,9 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   using W2 = Wpc2Cfg<T>;
   using SH = Shape<10>;
   using ST = Stockham<T, 10, INV, WC::S, WC::PS, true, 32, true>;
-  constexpr int E = SH::E, B = WC::B, BOX = WC::BOX, NBOX = WC::NBOX, KPB = E / NBOX, NR = 2 * NBOX;
-  static_assert(W2::OK && KPB == 8, "unsupported shape for the 2 x 1024 kernel");
+  constexpr int E = SH::E, B = WC::B, BOX = WC::BOX, NBOX = WC::NBOX, KPB = E / NBOX;
+  constexpr int NSLOT = W2::NSLOT, OROWS = W2::OROWS, NR = 2 * W2::NH / OROWS, KPR = OROWS / 32;  // rounds, values per round
+  static_assert(W2::OK && KPB == 8 && KPR == 4 && NR % (2 * NSLOT) == 0, "unsupported shape for the 2 x 1024 kernel");
 
   extern __shared__ __align__(1024) unsigned char smem_w2[];
   unsigned char* ring = smem_w2;
@@ -157,9 +164,9 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   uint64_t* full = bar;
   uint64_t* empty = bar + NBOX;
   uint64_t* xdrained = bar + 2 * NBOX;
-  uint64_t* ofull = bar + 2 * NBOX + 1;
-  uint64_t* oempty = bar + 2 * NBOX + 3;
-  volatile int* s_flag = reinterpret_cast<volatile int*>(bar + WC::NBAR);  // [2]
+  uint64_t* ofull = bar + 2 * NBOX + 1;           // [NSLOT]
+  uint64_t* oempty = bar + 2 * NBOX + 1 + NSLOT;  // [NSLOT]
+  volatile int* s_flag = reinterpret_cast<volatile int*>(bar + W2::NBAR);  // [2]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(const_cast<int*>(s_flag) + 2);
 
   const int t = threadIdx.x, w = t >> 5, tt = t & 31;
@@ -169,7 +176,7 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
       mbar_init(empty + q, B);
     }
     mbar_init(xdrained, B);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NSLOT; ++s) {
       mbar_init(ofull + s, B);
       mbar_init(oempty + s, 1);
     }
@@ -210,8 +217,7 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
         tma_load4(dst, &maps.ld, 2 * c0, h, q * BOX, grp, full + q, pol);
       }
     };
-    mbar_arrive(oempty + 0);  // the output stage starts empty
-    mbar_arrive(oempty + 1);
+    for (int s = 0; s < NSLOT; ++s) mbar_arrive(oempty + s);  // the output stage starts empty
     s_flag[0] = cur < prm.ntiles;
     if (cur >= prm.ntiles) {
       mbar_arrive(full + 0);
@@ -234,24 +240,26 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
       const int grp = (int)(cur / prm.tpg), c0 = (int)(cur % prm.tpg) * B;
 #pragma unroll 1
       for (int rr = 0; rr < NR; ++rr) {
-        const int s = rr & 1;
-        mbar_wait(ofull + s, (unsigned)((rr >> 1) & 1));  // slot s: four uses per tile
-        const unsigned char* src = xs + (size_t)s * WC::BOXB;
+        const int s = rr & (NSLOT - 1);
+        mbar_wait(ofull + s, (unsigned)((rr / NSLOT) & 1));  // slot s: NR / NSLOT (even) uses per tile
+        const unsigned char* src = xs + (size_t)s * W2::SLOTB;
         if (prm.nst > 1) {
           const int smask = (1 << prm.sst_shift) - 1;
-          for (int r = rr * BOX; r < (rr + 1) * BOX; r += prm.sbrows)
-            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - rr * BOX) * 128, pol);
+          for (int r = rr * OROWS; r < (rr + 1) * OROWS; r += prm.sbrows)
+            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - rr * OROWS) * 128, pol);
         } else {
-          tma_store3(&maps.st[0], 2 * c0, rr * BOX, grp, src, pol);
+          tma_store3(&maps.st[0], 2 * c0, rr * OROWS, grp, src, pol);
         }
         bulk_commit();
-        if (s == 1) {
-          bulk_wait_read1();
-          mbar_arrive(oempty + 0);
-          bulk_wait_read0();
-          mbar_arrive(oempty + 1);
+        if (rr >= 2) {  // the store of two rounds ago has read its slot
+          bulk_wait_read2();
+          mbar_arrive(oempty + ((rr - 2) & (NSLOT - 1)));
         }
       }
+      bulk_wait_read1();
+      mbar_arrive(oempty + ((NR - 2) & (NSLOT - 1)));
+      bulk_wait_read0();
+      mbar_arrive(oempty + ((NR - 1) & (NSLOT - 1)));
       if (!more) break;
       cur = nxt;
       nxt = dyn ? (long long)tk : nxt + step;
@@ -266,13 +274,12 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   const int lane_ofs = tt * 128 + (cchunk << 4) + (int)((w * sizeof(cx<T>)) & 15);
   // this lane's parking space: TMEM lane 32 (w % 4) + tt, NW columns from (w / 4) NW
   const uint32_t taddr = tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * W2::NW);
-  unsigned oe0 = 0, oe1 = 0;  // phases of oempty[0 / 1] consumed
-  unsigned g = 0;             // output-stage slot pairs begun (pair j is released by phase j + 1)
-  auto need = [&](int s, unsigned phase) {  // slot s has been read out for every pair before `phase`
-    if (s == 0) {
-      while (oe0 <= phase) { mbar_wait(oempty + 0, oe0 & 1u); ++oe0; }
-    } else {
-      while (oe1 <= phase) { mbar_wait(oempty + 1, oe1 & 1u); ++oe1; }
+  unsigned oe[NSLOT] = {0, 0, 0, 0};  // phases of oempty[s] consumed
+  unsigned g = 0;                     // uses of every slot begun in earlier tiles (use j is released by phase j + 1)
+  auto need = [&](int s, unsigned phase) {  // slot s has been read out for every use before `phase`
+    while (oe[s] <= phase) {
+      mbar_wait(oempty + s, oe[s] & 1u);
+      ++oe[s];
     }
   };
   for (unsigned it = 0;; ++it) {
@@ -293,8 +300,8 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
     }
     if (stop) break;
     ST::first(v, tt, s_tw);
-    need(0, g);  // the exchange buffer doubles as the output stage
-    need(1, g);
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) need(s, g);  // the exchange buffer doubles as the output stage
     auto hook = [&] {
       __syncwarp();
       if (h == 1 && tt == 0) mbar_arrive(xdrained);
@@ -307,31 +314,32 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
       continue;
     }
     mbar_wait(xdrained, (it >> 1) & 1u);
+    cx<T> e[8];
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
-      const int s = rr & 1;
-      need(s, g);
-      unsigned char* ob = xs + (size_t)s * WC::BOXB + lane_ofs;
-      if (rr < NBOX) {  // rows tt + 32 m, m = 8 rr + k: X[k] = E + w^k O; keep E - w^k O for round rr + 4
-        cx<T> e[8];
-        tmem_fetch8<T>(taddr + rr * W2::W8, e);
+      const int s = rr & (NSLOT - 1);
+      need(s, g + rr / NSLOT);
+      unsigned char* ob = xs + (size_t)s * W2::SLOTB + lane_ofs;
+      if (rr < NR / 2) {  // rows tt + 32 m, m = KPR rr + k: X[k] = E + w^k O; keep E - w^k O for round rr + NR / 2
+        if (rr % 2 == 0) tmem_fetch8<T>(taddr + (rr / 2) * W2::W8, e);
 #pragma unroll
-        for (int k = 0; k < KPB; ++k) {
-          const int m = rr * KPB + k;
+        for (int k = 0; k < KPR; ++k) {
+          const int m = rr * KPR + k;
+          const cx<T> ek = e[(rr % 2) * KPR + k];
           const cx<T> tw = ctw<INV>(v[m], s_w2[tt + 32 * m]);
-          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = cadd(e[k], tw);
-          v[m] = csub(e[k], tw);
+          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = cadd(ek, tw);
+          v[m] = csub(ek, tw);
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < KPB; ++k)
-          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = v[(rr - NBOX) * KPB + k];
+        for (int k = 0; k < KPR; ++k)
+          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = v[(rr - NR / 2) * KPR + k];
       }
       fence_async_shared();
       __syncwarp();
       if (tt == 0) mbar_arrive(ofull + s);
-      if (s == 1) ++g;
     }
+    g += NR / NSLOT;
   }
   // every consumer warp is done with tensor memory: warp 0 frees it
   tmem_fence_before();

@@ -179,8 +179,17 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #ifndef TFFFT_R2C_L9_F64_MB
 #define TFFFT_R2C_L9_F64_MB 4
 #endif
+// n2 = 2048 (the rows of BASELINE config 4), per 8.6 GB-in / 8.6 GB-out launch
+// (profiles/r02s4/rows_2048.txt): r2c 3.08 ms on the default radix 32 x 32,
+// 2.97 ms on radix 16 x 8 x 8, 3.11 ms on 8 x 8 x 4 x 4; c2r 3.90 / 3.70 / 3.45 ms
+#ifndef TFFFT_R2C_L10_F64_MB
+#define TFFFT_R2C_L10_F64_MB 4
+#endif
+#ifndef TFFFT_C2R_L10_F64_MB
+#define TFFFT_C2R_L10_F64_MB 3
+#endif
 __host__ __device__ constexpr int r2c_radix_bits(int L, int real_bytes) {
-  return (L == 9 && real_bytes == 8) ? TFFFT_R2C_L9_F64_MB : 0;
+  return real_bytes == 8 ? (L == 9 ? TFFFT_R2C_L9_F64_MB : (L == 10 ? TFFFT_R2C_L10_F64_MB : 0)) : 0;
 }
 // c2r likewise: radix 8 at 6 CTAs/SM, 3.14 ms per 1024^3 launch vs 3.23 ms
 // with radix 32x16 at 240 registers (profiles/r01s3/rows.txt)
@@ -190,7 +199,7 @@ __host__ __device__ constexpr int r2c_radix_bits(int L, int real_bytes) {
 // (and for n2 = 512: radix 8 at 5 CTAs/SM, 0.392 -> 0.379 ms per 512^3 launch;
 // the r2c rows there keep radix 16, profiles/r01s13/rows_512.txt)
 __host__ __device__ constexpr int c2r_radix_bits(int L, int real_bytes) {
-  return real_bytes == 8 ? (L == 9 ? TFFFT_C2R_L9_F64_MB : (L == 8 ? 3 : 0)) : 0;
+  return real_bytes == 8 ? (L == 9 ? TFFFT_C2R_L9_F64_MB : (L == 8 ? 3 : (L == 10 ? TFFFT_C2R_L10_F64_MB : 0))) : 0;
 }
 
 template <int L, int MB = 0> struct RowCfg {

@@ -608,7 +608,7 @@ static bool tma_cols_enabled(tffft_plan_t pl, int L) {
 // float32 stage-1b rows of an odd n2c (8 bytes off 16-byte alignment on odd rows)
 // stay on col_tma_kernel: a swizzled box must start on a 16-byte boundary (a box
 // started one complex in raised "illegal instruction" on the B200).
-// Measured on one box (profiles/r02/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
+// Measured on one box (profiles/r02s4/wpc_ab.txt): stage 1b 2.87 -> 2.57 ms per
 // float64 1024^3 launch; stage 3 (rows 8.4 MB apart) ties at 2.99-3.00 ms in
 // isolation and is slightly slower live, so it keeps col_tma_kernel.
 static int wpc_cols_mode() {
@@ -638,7 +638,8 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     return TFFFT_OK;
   // 2 x 1024: loads by row parity, sub-boxes of half rows within a block
   const long long lbrows = std::min<long long>(256, x2 ? j.ld_in_rows / 2 : j.ld_in_rows);
-  const long long srows_blk = two ? j.st_rows : n, sbrows = std::min<long long>(256, srows_blk);
+  const long long srows_blk = two ? j.st_rows : n;
+  const long long sbrows = std::min<long long>(x2 ? 128 : 256, srows_blk);  // 2 x 1024: 128-row output rounds
   // sub-boxes start on 1024-byte (8-row) boundaries of the swizzled landing boxes
   if (lbrows < 8 || sbrows < 8 || (two && srows_blk * (long long)j.st_tab.size() != n)) return TFFFT_OK;
   for (void* d : j.st_tab)
