@@ -57,27 +57,37 @@ __device__ __forceinline__ void bulk_wait_read2() { asm volatile("cp.async.bulk.
 template <typename T, int L>
 struct WpcCfg {
   using SH = Shape<L>;
-  static constexpr int N = SH::N, E = SH::E;
-  static constexpr int B = 128 / (int)sizeof(cx<T>);  // columns per tile: 128-byte rows
-  // B consumer warps + one producer warpgroup (four warps, one active thread).  A sub-partition holds 16 K
+  static constexpr int N = SH::N, E = SH::E, TPT = SH::TPT;
+  // columns per warp (1024 points: one; 512 points: two, a half-warp each) and 128-byte sub-boxes side by side
+  // in a row of the tile (512 points: two -- 256-byte row visits, as col_tma_kernel's 16 float64 columns)
+  static constexpr int CPW = 32 / TPT, NSIDE = CPW;
+  static constexpr int BS = 128 / (int)sizeof(cx<T>);  // columns of one sub-box
+  static constexpr int B = NSIDE * BS;                 // columns per tile
+  static constexpr int WARPS = B / CPW;                // consumer warps: 8 (float64), 16 (float32)
+  // WARPS consumer warps + one producer warpgroup (four warps, one active thread).  A sub-partition holds 16 K
   // registers and ends up with two (four) consumer warps and one producer warp: the CTA starts with the
   // uniform count of its launch bound and the roles trade registers with setmaxnreg (whole warpgroups).
-  static constexpr int THREADS = 32 * (B + 4);
+  static constexpr int THREADS = 32 * (WARPS + 4);
   // setmaxnreg.inc only hands out what the producers' setmaxnreg.dec released:
   // float64 128 x (168 - 40) = 256 x (232 - 168); float32 128 x (96 - 24) >= 512 x (112 - 96)
   static constexpr int CREG = sizeof(T) == 8 ? 232 : 112;  // consumers, after setmaxnreg.inc
   static constexpr int PREG = sizeof(T) == 8 ? 40 : 24;    // producer warpgroup, after setmaxnreg.dec
-  static constexpr int BOX = 256, NBOX = N / BOX;     // rows per TMA box (hardware limit 256)
+  static constexpr int BOX = 256, NQ = N / BOX;        // rows per TMA box (hardware limit 256), row blocks per tile
+  static constexpr int NBOX = NQ * NSIDE;              // ring boxes: box (q, side) at q NSIDE + side
   static constexpr size_t BOXB = (size_t)BOX * 128;
   static constexpr size_t RING = BOXB * NBOX;
-  static constexpr int PS = SH::EB;                   // one pad word per E words
-  static constexpr int S = N + (N >> PS);             // words per warp-private exchange region
+  static constexpr int KPB = E / NQ;                   // operands a lane takes from one row block
+  static constexpr int NROUND = 4, OROWS = N / NROUND; // output rounds; slot = NSIDE sub-boxes of OROWS rows
+  static constexpr size_t SLOTB = (size_t)NSIDE * OROWS * 128;
+  static constexpr int PS = SH::EB;                    // one pad word per E words
+  static constexpr int S = N + (N >> PS);              // words per column of the exchange buffer
   static constexpr size_t XS = sizeof(T) * (size_t)B * S;
   static constexpr int TW = SH::TW > 0 ? SH::TW : 1;
   static constexpr int NBAR = 2 * NBOX + 5;
   static constexpr size_t SMEM = RING + XS + sizeof(cx<T>) * TW + 8 * NBAR + 16;
-  static constexpr bool OK = SH::TPT == 32 && SH::P == 2 && NBOX >= 2 && 2 * BOXB <= XS && SMEM <= 227 * 1024 &&
-                             E % NBOX == 0 && SH::RL == E && SH::R0 == E;
+  static constexpr bool OK = (TPT == 32 || TPT == 16) && SH::P == 2 && NBOX == 4 && 2 * SLOTB <= XS &&
+                             SMEM <= 227 * 1024 && E % NQ == 0 && SH::R0 == E && E % NROUND == 0 &&
+                             (TPT * KPB) % 8 == 0 && OROWS % 32 == 0;
 };
 
 constexpr int kWpcMaps = 16;  // store maps (destination blocks, p <= 16)
@@ -109,7 +119,8 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   using WC = WpcCfg<T, L>;
   using SH = Shape<L>;
   using ST = Stockham<T, L, INV, WC::S, WC::PS, true, 32, true>;
-  constexpr int E = SH::E, B = WC::B, BOX = WC::BOX, NBOX = WC::NBOX, KPB = E / NBOX;  // operands per box
+  constexpr int E = SH::E, B = WC::B, BOX = WC::BOX, NBOX = WC::NBOX, NQ = WC::NQ, NSIDE = WC::NSIDE, KPB = WC::KPB;
+  constexpr int TPT = WC::TPT, WARPS = WC::WARPS, NROUND = WC::NROUND, OROWS = WC::OROWS, RL = SH::RL;
   static_assert(WC::OK, "unsupported shape for the warp-per-column kernel");
 
   extern __shared__ __align__(1024) unsigned char smem_wc[];
@@ -128,11 +139,11 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   if (t == 0) {
     for (int q = 0; q < NBOX; ++q) {
       mbar_init(full + q, 1);
-      mbar_init(empty + q, B);
+      mbar_init(empty + q, WARPS / NSIDE);  // the warps whose columns lie in this side of the tile
     }
-    mbar_init(xdrained, B);
+    mbar_init(xdrained, WARPS);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(ofull + s, B);
+      mbar_init(ofull + s, WARPS);
       mbar_init(oempty + s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -143,27 +154,27 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   }
   __syncthreads();
 
-  if (w >= B) {
+  if (w >= WARPS) {
     // ---------------- producer: every global access of the CTA ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(WC::PREG));
-    if (t != 32 * B) return;
+    if (t != 32 * WARPS) return;
     const uint64_t pol = prm.evict_first ? policy_evict_first() : policy_evict_normal();
     const bool dyn = prm.ticket != nullptr;
     const long long step = gridDim.x;
     long long cur = dyn ? (long long)atomicAdd(prm.ticket, 1ull) : (long long)blockIdx.x;
     long long nxt = dyn ? (long long)atomicAdd(prm.ticket, 1ull) : cur + step;
-    auto load_box = [&](long long tile, int q) {
-      const int grp = (int)(tile / prm.tpg), c0 = (int)(tile % prm.tpg) * B;
+    auto load_box = [&](long long tile, int bx) {  // box (q, side): rows [256 q, 256 q + 256), sub-box `side`
+      const int q = bx / NSIDE, side = bx % NSIDE;
+      const int grp = (int)(tile / prm.tpg), x0 = 2 * ((int)(tile % prm.tpg) * B + side * WC::BS);
       fence_async_shared();
-      mbar_arrive_tx(full + q, (unsigned)WC::BOXB);
-      unsigned char* dst = ring + (size_t)q * WC::BOXB;
+      mbar_arrive_tx(full + bx, (unsigned)WC::BOXB);
+      unsigned char* dst = ring + (size_t)bx * WC::BOXB;
       if (prm.load4) {  // two-level rows: sub-boxes never cross a block
         const int rmask = (1 << prm.lin_shift) - 1;
         for (int r = q * BOX; r < (q + 1) * BOX; r += prm.lbrows)
-          tma_load4(dst + (size_t)(r - q * BOX) * 128, &maps.ld, 2 * c0, r & rmask, r >> prm.lin_shift, grp, full + q,
-                    pol);
+          tma_load4(dst + (size_t)(r - q * BOX) * 128, &maps.ld, x0, r & rmask, r >> prm.lin_shift, grp, full + bx, pol);
       } else {
-        tma_load3(dst, &maps.ld, 2 * c0, q * BOX, grp, full + q, pol);
+        tma_load3(dst, &maps.ld, x0, q * BOX, grp, full + bx, pol);
       }
     };
     // the output stage starts empty
@@ -171,7 +182,7 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
     mbar_arrive(oempty + 1);
     s_flag[0] = cur < prm.ntiles;
     if (cur >= prm.ntiles) {
-      mbar_arrive(full + 0);
+      for (int side = 0; side < NSIDE; ++side) mbar_arrive(full + side);
       return;
     }
     for (int q = 0; q < NBOX; ++q) load_box(cur, q);
@@ -183,22 +194,26 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
       const bool more = nxt < prm.ntiles;
       s_flag[par ^ 1u] = more;
       for (int q = 0; q < NBOX; ++q) {
-        mbar_wait(empty + q, par);  // every warp holds its operands of box q
+        mbar_wait(empty + q, par);  // every warp of the side holds its operands of box q
         if (more) load_box(nxt, q);
-        else if (q == 0) mbar_arrive(full + 0);  // wake the consumers: no further tile
+        else if (q < NSIDE) mbar_arrive(full + q);  // wake the consumers (row block 0 of each side): no further tile
       }
       const int grp = (int)(cur / prm.tpg), c0 = (int)(cur % prm.tpg) * B;
 #pragma unroll
-      for (int qq = 0; qq < NBOX; ++qq) {
+      for (int qq = 0; qq < NROUND; ++qq) {
         const int s = qq & 1;
-        mbar_wait(ofull + s, (unsigned)(((it * (NBOX / 2)) + (qq >> 1)) & 1u));
-        const unsigned char* src = xs + (size_t)s * WC::BOXB;
-        if (prm.nst > 1) {  // block redirect: row r goes to row (r mod block rows) of st[r / block rows]
-          const int smask = (1 << prm.sst_shift) - 1;
-          for (int r = qq * BOX; r < (qq + 1) * BOX; r += prm.sbrows)
-            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - qq * BOX) * 128, pol);
-        } else {
-          tma_store3(&maps.st[0], 2 * c0, qq * BOX, grp, src, pol);
+        mbar_wait(ofull + s, (unsigned)(((it * (NROUND / 2)) + (qq >> 1)) & 1u));
+#pragma unroll
+        for (int side = 0; side < NSIDE; ++side) {
+          const unsigned char* src = xs + (size_t)s * WC::SLOTB + (size_t)side * OROWS * 128;
+          const int x0 = 2 * (c0 + side * WC::BS);
+          if (prm.nst > 1) {  // block redirect: row r goes to row (r mod block rows) of st[r / block rows]
+            const int smask = (1 << prm.sst_shift) - 1;
+            for (int r = qq * OROWS; r < (qq + 1) * OROWS; r += prm.sbrows)
+              tma_store3(&maps.st[r >> prm.sst_shift], x0, r & smask, grp, src + (size_t)(r - qq * OROWS) * 128, pol);
+          } else {
+            tma_store3(&maps.st[0], x0, qq * OROWS, grp, src, pol);
+          }
         }
         bulk_commit();
         if (s == 1) {
@@ -216,27 +231,31 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
     return;
   }
 
-  // ---------------- consumers: warp w owns column w of every tile ----------------
+  // ---------------- consumers: warp w owns columns w CPW .. of every tile ----------------
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WC::CREG));
-  // chunk of column w in a row congruent to tt mod 8 (128-byte swizzle)
-  const int cchunk = (int)((w * sizeof(cx<T>)) >> 4) ^ (tt & 7);
-  const int lane_ofs = tt * 128 + (cchunk << 4) + (int)((w * sizeof(cx<T>)) & 15);
+  const int tl = tt % TPT;                    // lane within its transform
+  const int c = w * WC::CPW + tt / TPT;       // this lane's column of the tile
+  const int cb = c * (int)sizeof(cx<T>);      // byte offset of the column in a tile row
+  const int side = cb >> 7;
+  // chunk of the column in a row congruent to tl mod 8 (128-byte swizzle)
+  const int lane_ofs = tl * 128 + ((((cb & 127) >> 4) ^ (tl & 7)) << 4) + (cb & 15);
   unsigned oe = 0;  // phases of oempty[s] consumed (the same count for both slots)
   for (unsigned it = 0;; ++it) {
     const unsigned par = it & 1u;
     cx<T> v[E];
 #pragma unroll
-    for (int q = 0; q < NBOX; ++q) {
-      mbar_wait(full + q, par);
+    for (int q = 0; q < NQ; ++q) {
+      const int bx = q * NSIDE + side;
+      mbar_wait(full + bx, par);
       if (q == 0 && !s_flag[par]) return;
-      const unsigned char* bx = ring + (size_t)q * WC::BOXB + lane_ofs;
+      const unsigned char* bxp = ring + (size_t)bx * WC::BOXB + lane_ofs;
 #pragma unroll
-      for (int k = 0; k < KPB; ++k)  // row tt + 32 (q KPB + k) = box q, row tt + 32 k
-        v[SH::in_slot(q * KPB + k)] = *reinterpret_cast<const cx<T>*>(bx + (size_t)k * 32 * 128);
+      for (int k = 0; k < KPB; ++k)  // row tl + TPT (q KPB + k) = row block q, row tl + TPT k
+        v[SH::in_slot(q * KPB + k)] = *reinterpret_cast<const cx<T>*>(bxp + (size_t)k * TPT * 128);
       __syncwarp();
-      if (tt == 0) mbar_arrive(empty + q);
+      if (tt == 0) mbar_arrive(empty + bx);
     }
-    ST::first(v, tt, s_tw);
+    ST::first(v, tl, s_tw);
     // the exchange buffer doubles as the output stage: both slots read out
     mbar_wait(oempty + 0, oe & 1u);
     mbar_wait(oempty + 1, oe & 1u);
@@ -245,19 +264,22 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
       __syncwarp();
       if (tt == 0) mbar_arrive(xdrained);
     };
-    ST::finish(xs, v, tt, w, s_tw, hook);
+    ST::finish(xs, v, tl, c, s_tw, hook);
     mbar_wait(xdrained, par);  // every warp is out of the exchange buffer
 #pragma unroll
-    for (int qq = 0; qq < NBOX; ++qq) {
+    for (int qq = 0; qq < NROUND; ++qq) {
       const int s = qq & 1;
       if (qq >= 2) {
         mbar_wait(oempty + s, oe & 1u);
         if (s == 1) ++oe;
       }
-      unsigned char* ob = xs + (size_t)s * WC::BOXB + lane_ofs;
+      unsigned char* ob = xs + (size_t)s * WC::SLOTB + (size_t)side * OROWS * 128 + lane_ofs;
+      // output row tl + TPT u + (N / RL) m in v[u RL + m]: the rows of round qq are m in [qq RL / 4, (qq + 1) RL / 4)
 #pragma unroll
-      for (int k = 0; k < KPB; ++k)  // output row tt + 32 m, m = qq KPB + k (RL = E: v[m])
-        *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = v[qq * KPB + k];
+      for (int u = 0; u < E / RL; ++u)
+#pragma unroll
+        for (int m = 0; m < RL / NROUND; ++m)
+          *reinterpret_cast<cx<T>*>(ob + (size_t)(TPT * u + (SH::N / RL) * m) * 128) = v[u * RL + qq * (RL / NROUND) + m];
       fence_async_shared();  // the TMA store reads the stage through the async proxy
       __syncwarp();
       if (tt == 0) mbar_arrive(ofull + s);
@@ -265,8 +287,8 @@ col_wpc_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   }
 }
 
-// 1024-point columns; 2048-point columns as 2 x 1024 (col_wpc2.cuh)
-__host__ __device__ constexpr bool col_wpc_supported(int L) { return L == 10 || L == 11; }
+// 512- and 1024-point columns; 2048-point columns as 2 x 1024 (col_wpc2.cuh)
+__host__ __device__ constexpr bool col_wpc_supported(int L) { return L == 9 || L == 10 || L == 11; }
 
 template <typename T>
 cudaError_t launch_col_wpc(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s);

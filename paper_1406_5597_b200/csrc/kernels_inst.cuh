@@ -392,6 +392,7 @@ static cudaError_t wpc2_one(const WpcMaps& maps, const WpcParams& p, cudaStream_
 template <>
 cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const WpcMaps& maps, const WpcParams& p, cudaStream_t s) {
   if (L == 11) return inv ? wpc2_one<TFFFT_REAL, true>(maps, p, s) : wpc2_one<TFFFT_REAL, false>(maps, p, s);
+  if (L == 9) return inv ? wpc_one<TFFFT_REAL, 9, true>(maps, p, s) : wpc_one<TFFFT_REAL, 9, false>(maps, p, s);
   if (L != 10) return cudaErrorInvalidValue;
   return inv ? wpc_one<TFFFT_REAL, 10, true>(maps, p, s) : wpc_one<TFFFT_REAL, 10, false>(maps, p, s);
 }
@@ -399,6 +400,7 @@ cudaError_t launch_col_wpc<TFFFT_REAL>(int L, bool inv, const WpcMaps& maps, con
 template <>
 int col_wpc_width<TFFFT_REAL>(int L) {
   if (L == 11) return Wpc2Cfg<TFFFT_REAL>::OK ? WpcCfg<TFFFT_REAL, 10>::B : 0;
+  if (L == 9) return WpcCfg<TFFFT_REAL, 9>::OK ? WpcCfg<TFFFT_REAL, 9>::B : 0;
   return L == 10 && WpcCfg<TFFFT_REAL, 10>::OK ? WpcCfg<TFFFT_REAL, 10>::B : 0;
 }
 

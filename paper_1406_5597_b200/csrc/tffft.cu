@@ -626,7 +626,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
   *done = false;
   const int mode = wpc_cols_mode();
   const bool x2 = L == 11;  // 2048 points as 2 x 1024 (col_wpc2.cuh): every pass, col_fft_kernel is far slower there
-  if (!(mode == 1 || (mode == 2 && (!j.wide || pl->dtype == TFFFT_F32 || x2))) || !col_wpc_supported(L))
+  if (!(mode == 1 || (mode == 2 && (!j.wide || pl->dtype == TFFFT_F32 || x2 || L == 9))) || !col_wpc_supported(L))
     return TFFFT_OK;
   if (x2 && (!pl->tw10 || !pl->twh11 || j.ld_in_rows % 2)) return TFFFT_OK;
   const long long esz = (long long)pl->esz, n = 1LL << L;
@@ -639,7 +639,9 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
   // 2 x 1024: loads by row parity, sub-boxes of half rows within a block
   const long long lbrows = std::min<long long>(256, x2 ? j.ld_in_rows / 2 : j.ld_in_rows);
   const long long srows_blk = two ? j.st_rows : n;
-  const long long sbrows = std::min<long long>(x2 ? 128 : 256, srows_blk);  // 2 x 1024: 128-row output rounds
+  // rows per output round: a quarter of the column (2 x 1024: 128-row rounds)
+  const long long sbrows = std::min<long long>(x2 ? 128 : n / 4, srows_blk);
+  const cuuint32_t boxw = (cuuint32_t)(256 / esz);  // reals in a 128-byte sub-box row
   // sub-boxes start on 1024-byte (8-row) boundaries of the swizzled landing boxes
   if (lbrows < 8 || sbrows < 8 || (two && srows_blk * (long long)j.st_tab.size() != n)) return TFFFT_OK;
   for (void* d : j.st_tab)
@@ -650,7 +652,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     cuuint64_t d[4] = {(cuuint64_t)(2 * j.cols), 2, (cuuint64_t)(n / 2), (cuuint64_t)j.ngrp};
     cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
-    cuuint32_t box[4] = {(cuuint32_t)(2 * B), 1, 256, 1};
+    cuuint32_t box[4] = {boxw, 1, 256, 1};
     TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else if (x2) {  // (cols, parity, half rows within a block, blocks, groups)
@@ -658,13 +660,13 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
                        (cuuint64_t)j.ngrp};
     cuuint64_t st[4] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
-    cuuint32_t box[5] = {(cuuint32_t)(2 * B), 1, (cuuint32_t)lbrows, 1, 1};
+    cuuint32_t box[5] = {boxw, 1, (cuuint32_t)lbrows, 1, 1};
     TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 5, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else if (j.ld_blocks == 1) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)n, (cuuint64_t)j.ngrp};
     cuuint64_t st[2] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
-    cuuint32_t box[3] = {(cuuint32_t)(2 * B), 256, 1};
+    cuuint32_t box[3] = {boxw, 256, 1};
     TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else {
@@ -672,7 +674,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
                        (cuuint64_t)j.ngrp};
     cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
-    cuuint32_t box[4] = {(cuuint32_t)(2 * B), (cuuint32_t)lbrows, 1, 1};
+    cuuint32_t box[4] = {boxw, (cuuint32_t)lbrows, 1, 1};
     TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B));
   }
@@ -681,7 +683,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)srows_blk, (cuuint64_t)j.ngrp};
     cuuint64_t st[2] = {(cuuint64_t)(j.st_in * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.st_g * esz : srows_blk * j.st_in * esz)};
-    cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)sbrows, 1};
+    cuuint32_t box[3] = {boxw, (cuuint32_t)sbrows, 1};
     TRY(make_map(pl, &maps.st[q], two ? j.st_tab[q] : j.st_base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_SWIZZLE_128B));
   }

@@ -426,14 +426,18 @@ def test_tma_column_kernel_bitwise(shape, p, dtype):
 
 
 WPC_CASES = [((1024, 16, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((16, 1024, 64), 1),
-             ((32, 1024, 16), 2), ((32, 1024, 16), 4), ((64, 1024, 16), 8), ((16, 1024, 8), 16)]
+             ((32, 1024, 16), 2), ((32, 1024, 16), 4), ((64, 1024, 16), 8), ((16, 1024, 8), 16),
+             ((1024, 64, 16), 2), ((1024, 32, 16), 8),
+             ((512, 16, 8), 1), ((8, 512, 16), 1), ((512, 512, 8), 1), ((32, 512, 16), 4), ((512, 64, 16), 2),
+             ((512, 32, 16), 8), ((16, 512, 8), 16)]
 
 
 @pytest.mark.parametrize("shape,p", WPC_CASES, ids=lambda v: str(v))
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_wpc_column_kernel_bitwise(shape, p, dtype, monkeypatch):
-    """Warp-per-column kernel (col_wpc.cuh, 1024-point columns): one warp owns
-    a column, operands from the swizzled TMA landing ring, outputs through TMA
+    """Warp-per-column kernel (col_wpc.cuh, 1024-point columns, and 512-point
+    columns two per warp with two sub-boxes side by side): one warp owns a
+    column, operands from the swizzled TMA landing ring, outputs through TMA
     stores.  Same engine and twiddles as col_tma_kernel, so with it on every
     1024-point pass (TFFFT_WPC=1), on the stage-1b passes only (the default,
     2) or off (0) the spectra and inverse outputs are bitwise identical, and
