@@ -616,6 +616,19 @@ static int wpc_cols_mode() {
   return e ? atoi(e) : 2;
 }
 
+// L2 promotion of the column-pass load maps (TFFFT_TMA_PROMO: 0 none (default), 1 = 64, 2 = 128, 3 = 256 bytes;
+// applied to the wide passes only, whose 128-byte row visits sit in 256-byte-aligned pairs)
+static CUtensorMapL2promotion col_promo(bool wide) {
+  static const int v = [] {
+    const char* e = getenv("TFFFT_TMA_PROMO");
+    return e ? atoi(e) : 0;
+  }();
+  if (!wide) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  return v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                         : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
 // Column pass through the warp-per-column kernel: loads as columns_tma_two
 // describes them (3D map, or 4D over the landing bands), stores uniform
 // (st_tab empty: row r of the column at st_base + r * st_in) or one map per
@@ -653,7 +666,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
     cuuint32_t box[4] = {boxw, 1, 256, 1};
-    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, col_promo(j.wide),
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else if (x2) {  // (cols, parity, half rows within a block, blocks, groups)
     cuuint64_t d[5] = {(cuuint64_t)(2 * j.cols), 2, (cuuint64_t)(j.ld_in_rows / 2), (cuuint64_t)j.ld_blocks,
@@ -661,13 +674,13 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     cuuint64_t st[4] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(2 * j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
     cuuint32_t box[5] = {boxw, 1, (cuuint32_t)lbrows, 1, 1};
-    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 5, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 5, d, st, box, col_promo(j.wide),
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else if (j.ld_blocks == 1) {
     cuuint64_t d[3] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)n, (cuuint64_t)j.ngrp};
     cuuint64_t st[2] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : n * j.ld_in * esz)};
     cuuint32_t box[3] = {boxw, 256, 1};
-    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 3, d, st, box, col_promo(j.wide),
                  CU_TENSOR_MAP_SWIZZLE_128B));
   } else {
     cuuint64_t d[4] = {(cuuint64_t)(2 * j.cols), (cuuint64_t)j.ld_in_rows, (cuuint64_t)j.ld_blocks,
@@ -675,7 +688,7 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
     cuuint64_t st[3] = {(cuuint64_t)(j.ld_in * esz), (cuuint64_t)(j.ld_out * esz),
                         (cuuint64_t)(j.ngrp > 1 ? j.ld_g * esz : j.ld_blocks * j.ld_out * esz)};
     cuuint32_t box[4] = {boxw, (cuuint32_t)lbrows, 1, 1};
-    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+    TRY(make_map(pl, &maps.ld, const_cast<void*>(j.ld_base), 4, d, st, box, col_promo(j.wide),
                  CU_TENSOR_MAP_SWIZZLE_128B));
   }
   const int nst = two ? (int)j.st_tab.size() : 1;
@@ -744,7 +757,7 @@ static int columns_tma(tffft_plan_t pl, int L, bool inv, bool wide, void* base, 
     cuuint64_t d[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)n, (cuuint64_t)ngrp};
     cuuint64_t st[2] = {(cuuint64_t)rbytes, (cuuint64_t)gbytes};
     cuuint32_t box[3] = {(cuuint32_t)(2 * B), (cuuint32_t)std::min<long long>(n, 256), 1};
-    TRY(make_map(pl, &map, base, 3, d, st, box, CU_TENSOR_MAP_L2_PROMOTION_NONE));
+    TRY(make_map(pl, &map, base, 3, d, st, box, col_promo(wide)));
     map_odd = map;
   } else {
     // odd rows miss 16-byte alignment by `mis` = one complex: their boxes start
