@@ -13,8 +13,11 @@ Configs (BASELINE.json): 512^3 float64 standard normal at p = 1, 2, 4 (p > 1
 on the local fabric: p ranks on one GPU); 1024^3 float64 and float32 uniform
 at p = 1 (the headline bench configuration; float32 gets the fp32-rounded
 input); the turbulence field (3 components, inverse
-then forward) at 256^3 for p = 1, 2.  Comparisons run on the GPU (torch) to
-keep the 8.6 GB buffers off the host's single-threaded numpy paths.
+then forward) at 256^3 for p = 1, 2; and the per-rank shapes of 2048^3
+over 8 ranks (config 4, which does not fit one GPU as a whole): 256 x 2048 x
+2048 (rows of 2048, n1 = 2048 columns) and 2048 x 256 x 2048 (n0 = 2048
+columns) at p = 1.  Comparisons run on the GPU (torch) to keep the 8.6 GB
+buffers off the host's single-threaded numpy paths.
 """
 
 import os
@@ -89,6 +92,29 @@ def test_1024_cubed_p1_vs_oracle(dtype):
     fp.close()
     assert e_fwd <= TOL[dtype], e_fwd
     assert e_rt <= TOL[dtype], e_rt
+
+
+@pytest.mark.parametrize("shape", [(256, 2048, 2048), (2048, 256, 2048)], ids=lambda v: "x".join(map(str, v)))
+def test_2048_rank_shapes_p1_vs_oracle(shape):
+    """BASELINE config 4 (2048^3 at p = 4, 8) per rank: the 8.6 GB real slab of
+    one of 8 ranks.  2048-point rows and the 2 x 1024 tensor-memory column
+    kernel (col_wpc2.cuh) on n1 (first shape) and on n0 (second shape), against
+    the oracle at full size."""
+    x = oracle.uniform_field(shape, seed=13)
+    ref = oracle.forward_all(x, 1, workers=WORKERS)[0]
+    grid = tf.GlobalGrid(*shape)
+    ep = tf.make_communicators(1)[0]
+    fp = tf.plan(grid, ep, tf.Strategy.STRIDED)
+    slab = tf.scatter_real(x, grid, 1)[0]
+    del x
+    spec = tf.forward(fp, slab)
+    e_fwd = rel_dev(spec.data, ref)
+    del ref
+    back = tf.inverse(fp, spec)
+    e_rt = rel_dev(back.data, slab.data)
+    fp.close()
+    assert e_fwd <= 1e-12, e_fwd
+    assert e_rt <= 1e-12, e_rt
 
 
 @pytest.fixture(scope="module")
