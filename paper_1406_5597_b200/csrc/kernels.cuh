@@ -173,6 +173,13 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #ifndef TFFFT_R2C_MINB9
 #define TFFFT_R2C_MINB9 8
 #endif
+// (c2r at 5 CTAs/SM: 3.44 -> 3.34 ms per 256x2048x2048 launch, profiles/r02s4/rows_2048.txt)
+#ifndef TFFFT_C2R_MINB10
+#define TFFFT_C2R_MINB10 5
+#endif
+#ifndef TFFFT_R2C_MINB10
+#define TFFFT_R2C_MINB10 1
+#endif
 // r2c row schedule: float64 rows of n2 = 1024 run the radix-8 schedule
 // (3 passes, E = 8, 6 CTAs/SM: 3.10 ms per 1024^3 launch vs 3.62 ms with radix
 // 32x16); every other row / column transform uses the default schedule
@@ -216,8 +223,10 @@ template <int L, int MB = 0> struct RowCfg {
   // pair loads -- at 5 (94 registers, 2.88 ms).  Other lengths keep the default.
   // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
   static constexpr bool CAP = (L == 9 || L == 8) && THREADS == 128 && Shape<L, MB>::E == 8;
-  static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : TFFFT_ROW_MINB;
-  static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : TFFFT_ROW_MINB;
+  // n2 = 2048 on the radix-8 schedule (E = 8, one row per 128-thread CTA): TFFFT_R2C_MINB10 / TFFFT_C2R_MINB10
+  static constexpr bool CAP10 = L == 10 && THREADS == 128 && Shape<L, MB>::E == 8;
+  static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : (CAP10 ? TFFFT_C2R_MINB10 : TFFFT_ROW_MINB);
+  static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : (CAP10 ? TFFFT_R2C_MINB10 : TFFFT_ROW_MINB);
 };
 
 template <typename T, int L, bool WIDE = false>

@@ -1,8 +1,9 @@
 #!/bin/bash
-# n2 = 2048 row kernels (BASELINE config 4's per-rank rows): radix schedule variants, ncu launch lists
-OUT=gpurun_out/${1:-rows10}
+# n2 = 2048 row kernels (BASELINE config 4's per-rank rows): radix schedule / occupancy variants, ncu launch lists
+# usage: bash tools/gpu_rows10.sh <outdir> <variant> ...   (variants under build/variants; "base" = the in-tree library)
+OUT=gpurun_out/${1:-rows10}; shift
 mkdir -p $OUT
-for v in base rows10_4 rows10_3; do
+for v in "$@"; do
   LIB=build/variants/$v/libtffft.so
   [ $v = base ] && LIB=paper_1406_5597_b200/libtffft.so
   TFFFT_LIB=$LIB timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
