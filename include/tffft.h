@@ -118,9 +118,11 @@ enum {
                                      exchanged (on the plan's exchange stream) while the next chunk computes;
                                      the default on NCCL communicators (TFFFT_XCHUNKS chunks, default 4),
                                      opt-in on the local fabric and IPC */
-  TFFFT_FLAG_TMA_COLUMNS = 16     /* column passes of length 512 / 1024 fed by TMA box copies (col_tma.cuh,
-                                     any p), the default (flags < 0) unless TFFFT_TMA_COLS=0; explicit
-                                     flags without it select the cp.async column kernel */
+  TFFFT_FLAG_TMA_COLUMNS = 16     /* column passes of length 512 / 1024 / 2048 fed by TMA box copies: the
+                                     warp-per-column kernels (col_wpc.cuh; 2048 points as 2 x 1024 through
+                                     tensor memory, col_wpc2.cuh) and col_tma.cuh, any p; the default
+                                     (flags < 0) unless TFFFT_TMA_COLS=0 (TFFFT_WPC picks among them);
+                                     explicit flags without it select the cp.async column kernel */
 };
 /* as tffft_plan_create with explicit algorithm flags; flags < 0 = environment defaults */
 int tffft_plan_create_ex(int n0, int n1, int n2, int dtype, int pattern, int flags, tffft_comm_t comm,

@@ -1,6 +1,6 @@
-// Warp-per-column, warp-specialised column c2c for sm_100a (1024-point columns:
-// stages 1b / 1b' / 3 / 3' at p = 1, and the two-level stage-1b / 1b' passes at
-// p > 1 -- band-redirected stores, landing-band loads).
+// Warp-per-column, warp-specialised column c2c for sm_100a (1024-point columns,
+// and 512-point columns two per warp: stages 1b / 1b' / 3 / 3' at p = 1, and
+// the two-level passes at p > 1 -- band-redirected stores, landing-band loads).
 //
 // col_tma_kernel (col_tma.cuh) spreads every column over all warps of the CTA
 // (thread = 4 rows x 8 columns slices), so the operand read, both FFT passes,
@@ -9,16 +9,18 @@
 // way round (profiles/r02/stage3_full.txt: exchange barriers 15% and the store
 // phase 19% of the stall samples).  Here a column belongs to ONE warp:
 //
-//   warps 0..B-1 (consumers): warp w owns column w of the tile; lane tt holds
-//       rows tt + 32 kk.  Operands come out of the TMA landing ring, the single
-//       Stockham exchange runs in a warp-private buffer behind __syncwarp, the
-//       results go into a shared output stage.  No CTA barrier in the loop:
-//       the warps drift apart, so one warp's FP64 pass overlaps another's
-//       shared-memory traffic.
-//   warp B (producer, one thread of a four-warp group): owns all global traffic.  It takes tiles
-//       from the ticket counter, refills each 256-row box of the landing ring
-//       as soon as every consumer has read it (cp.async.bulk.tensor loads), and
-//       sends every finished output quarter with a cp.async.bulk.tensor store.
+//   consumer warps: warp w owns column w of the tile; lane tt holds rows
+//       tt + 32 kk (512 points: two columns per warp, a half-warp each, a
+//       tile row being two 128-byte sub-boxes side by side).  Operands come
+//       out of the TMA landing ring, the single Stockham exchange runs in a
+//       warp-private buffer behind __syncwarp, the results go into a shared
+//       output stage.  No CTA barrier in the loop: the warps drift apart, so
+//       one warp's FP64 pass overlaps another's shared-memory traffic.
+//   producer (one thread of a four-warp group behind the consumers): owns
+//       all global traffic.  It takes tiles from the ticket counter, refills
+//       each 256-row box of the landing ring as soon as every consumer has
+//       read it (cp.async.bulk.tensor loads), and sends every finished output
+//       quarter with a cp.async.bulk.tensor store.
 //
 // The boxes use the 128-byte TMA swizzle: row r of a box keeps its 16-byte
 // chunk c at chunk position c ^ (r mod 8).  Lane tt reads rows congruent to
