@@ -482,15 +482,22 @@ r2c_rows_kernel(const RowParams prm) {
   // so each thread reads every pair once and writes both bins.
   cx<T>* out = reinterpret_cast<cx<T>*>(prm.spec) + row * prm.n2c;
   const T half = T(0.5);
-  auto pair = [&](int k) {
+  // The twiddle of k = tt + TPT q factors as w^tt * exp(-2 pi i q / (2 E)): one
+  // table load per thread and a rotation by a 16th (E = 8) or 32nd (E = 16)
+  // root of unity that is a constant after unrolling (float64; the kernel is
+  // bound by L1/TEX requests, profiles/r02s4/rows_full.txt).
+  constexpr bool ROT = sizeof(T) == 8 && (SH::E == 8 || SH::E == 16);
+  auto pair = [&](int k, cx<T> w) {
     const cx<T> A = zr[k];
     const cx<T> Bz = zr[N - k];
     const cx<T> S = {A.x + Bz.x, A.y - Bz.y};   // A + conj(B)
     const cx<T> D = {A.x - Bz.x, A.y + Bz.y};   // A - conj(B)
-    const cx<T> Tt = cmul(D, ldg_cx(twp + k));
+    const cx<T> Tt = cmul(D, w);
     out[k] = cx<T>{half * (S.x + Tt.y), half * (S.y - Tt.x)};
     if (N - k != k) out[N - k] = cx<T>{half * (S.x - Tt.y), -half * (S.y + Tt.x)};
   };
+  cx<T> wb = {T(1), T(0)};
+  if constexpr (ROT) wb = ldg_cx(twp + tt);
 #pragma unroll
   for (int q = 0; q < (SH::E > 1 ? SH::E / 2 : 1); ++q) {
     const int k = tt + SH::TPT * q;  // k < N/2
@@ -498,11 +505,13 @@ r2c_rows_kernel(const RowParams prm) {
       const cx<T> z0 = zr[0];
       out[0] = cx<T>{z0.x + z0.y, T(0)};
       out[N] = cx<T>{z0.x - z0.y, T(0)};
+    } else if constexpr (ROT) {
+      pair(k, SH::E == 8 ? mul_w16<false>(wb, q) : mul_w32<false>(wb, q));
     } else {
-      pair(k);
+      pair(k, ldg_cx(twp + k));
     }
   }
-  if (tt == 0 && N >= 2) pair(N / 2);  // the self-paired middle bin
+  if (tt == 0 && N >= 2) pair(N / 2, ldg_cx(twp + N / 2));  // the self-paired middle bin
 }
 
 // ---------------------------------------------------------------------------
@@ -559,12 +568,29 @@ c2r_rows_kernel(const RowParams prm) {
     const cx<T> Tt = cmulc(D, ldg_cx(twp + k)); // exp(+2 pi i k / n2) * D
     return {S.x - Tt.y, S.y + Tt.x};
   };
+  // The same with the twiddle factored: k = (tt + TPT u) + m N / R0, so
+  // exp(2 pi i k / n2) = exp(2 pi i (tt + TPT u) / n2) * exp(2 pi i m / (2 R0)):
+  // one table load per thread and u, and a rotation of D by a 16th (R0 = 8) or
+  // 32nd (R0 = 16) root of unity that is a compile-time constant after
+  // unrolling.  The kernel is bound by L1/TEX requests (85% busy,
+  // profiles/r02s4/rows_full.txt): this drops one of the three 16-byte loads
+  // per operand.
+  constexpr bool ROT = sizeof(T) == 8 && (SH::R0 == 8 || SH::R0 == 16);
+  auto pre_rot = [&](cx<T> A, cx<T> Bx, cx<T> wb, int m) -> cx<T> {
+    const cx<T> S = {A.x + Bx.x, A.y - Bx.y};
+    const cx<T> D = {A.x - Bx.x, A.y + Bx.y};
+    const cx<T> Dm = SH::R0 == 8 ? mul_w16<true>(D, m) : mul_w32<true>(D, m);
+    const cx<T> Tt = cmulc(Dm, wb);
+    return {S.x - Tt.y, S.y + Tt.x};
+  };
   cx<T> v[SH::E];
   if constexpr (sizeof(T) == 8) {
     // float64 (radix-8 schedule): pairs straight from global memory, 1024^3
     // launch 3.14 -> 2.97 ms against staging the row in shared memory
 #pragma unroll
-    for (int u = 0; u < SH::E / SH::R0; ++u)
+    for (int u = 0; u < SH::E / SH::R0; ++u) {
+      cx<T> wb = {T(1), T(0)};
+      if constexpr (ROT) wb = ldg_cx(twp + tt + SH::TPT * u);
 #pragma unroll
       for (int m = 0; m < SH::R0; ++m) {
         const int k = SH::in_elem(tt, u, m);
@@ -581,8 +607,10 @@ c2r_rows_kernel(const RowParams prm) {
         } else {
           Bx = ldg_cx(in + (N - k));
         }
-        v[u * SH::R0 + m] = pre(A, Bx, k);
+        if constexpr (ROT) v[u * SH::R0 + m] = pre_rot(A, Bx, wb, m);
+        else v[u * SH::R0 + m] = pre(A, Bx, k);
       }
+    }
   } else {
     // float32 (radix-32 schedule): the row staged in shared memory in natural
     // order, UNPADDED (reversed runs N - k stay bank-conflict free); 1.43 ms
