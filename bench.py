@@ -222,6 +222,22 @@ def full_pair_record():
         return None
 
 
+def stage3_kernel_name(n0: int, dt: str) -> str:
+    """The kernel the library runs for the stage-3 column pass by default (csrc/tffft.cu columns_wpc /
+    columns_tma): float64 1024-point columns keep col_tma_kernel; 512-point, float32 1024-point and
+    2048-point columns run the warp-per-column kernels; other lengths col_fft_kernel."""
+    if os.environ.get("TFFFT_TMA_COLS") == "0":
+        return "col_fft_kernel"
+    wpc = os.environ.get("TFFFT_WPC", "2")
+    if n0 == 2048 and wpc != "0":
+        return "col_wpc2_kernel"
+    if n0 == 512 and wpc != "0":
+        return "col_wpc_kernel"
+    if n0 == 1024:
+        return "col_wpc_kernel" if (wpc == "1" or (wpc == "2" and dt == "float32")) else "col_tma_kernel"
+    return "col_tma_kernel" if n0 == 512 else "col_fft_kernel"
+
+
 def cube_config(n0, n1, n2, dt, p):
     """The config object both arms print (identical keys and values)."""
     s_r = 8 if dt == "float64" else 4
@@ -427,8 +443,7 @@ def run_gpu(args):
             "roundtrip_rel_l2": rt,
         },
         "roofline": {"bound": "hbm",
-                     "kernel": (("col_tma_kernel" if p == 1 and n0 in (512, 1024) else "col_fft_kernel")
-                                + " (stage 3 strided n0 c2c)"),
+                     "kernel": stage3_kernel_name(n0, dt) + " (stage 3 strided n0 c2c)",
                      "achieved": ach, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach / hbm_peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": st3},
