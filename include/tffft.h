@@ -185,6 +185,11 @@ int tffft_reset_instrumentation(tffft_plan_t plan);
  * largest discarded imaginary magnitude and TFFFT_ERR_CONSISTENCY when a plane
  * violates the reference tolerance 1e-9*n2*max|X| (kernels.py:223-238). */
 int tffft_consistency(tffft_plan_t plan, double* residue);
+/* diagnostic: the exchange's NCCL calls (grouped ncclSend / ncclRecv, ncclAlltoAll when the loaded NCCL has it,
+ * the one-int ncclAllReduce barrier, the async-error poll) as a ONE-rank loopback on `device`, `count` real
+ * elements of `dtype`; received data must equal what was sent.  As much of the NCCL path (exchange.py:263-290
+ * over transport.py:359-419) as a one-GPU box can execute: NCCL refuses two ranks on one device. */
+int tffft_nccl_loopback(int device, long long count, int dtype, int* ran_alltoall);
 /* debug: fill the plan's exchange staging / landing buffers and c2r row
  * records with 0xFF bytes (NaN), so a read of an element no stage wrote shows
  * up as NaN in the output; synchronous */

@@ -15,6 +15,6 @@ from .fields import forward_batch, inverse_batch, radial_wavenumber, turbulence_
 from .layout import (DistAxis, GlobalGrid, RealSlab, SlabLayout, SpectralSlab, SpectralTag,
                      TwoLevelStride, column_stride_descriptor, owned_range, spectral_offset, validate)
 from .transport import (CommMode, CommPattern, CopyCounter, Endpoint, allgather_handles, init_ipc_endpoint,
-                        init_nccl_endpoint, make_communicators, run_spmd)
+                        init_nccl_endpoint, make_communicators, nccl_loopback, run_spmd)
 
 __version__ = "0.1.0"

@@ -40,6 +40,7 @@ _SIGS = {
                                              _c.c_int, _c.c_void_p, _c.POINTER(_c.c_void_p)]),
     "tffft_plan_batch": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "tffft_plan_poison": (_c.c_int, [_c.c_void_p]),
+    "tffft_nccl_loopback": (_c.c_int, [_c.c_int, _c.c_longlong, _c.c_int, _c.POINTER(_c.c_int)]),
     "tffft_plan_ipc_blob_bytes": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_size_t)]),
     "tffft_plan_ipc_export": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "tffft_plan_ipc_attach": (_c.c_int, [_c.c_void_p, _c.c_char_p]),

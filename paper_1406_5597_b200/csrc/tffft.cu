@@ -2322,6 +2322,100 @@ int tffft_plan_poison(tffft_plan_t pl) {
   return TFFFT_OK;
 }
 
+// Diagnostic: the exchange's NCCL calls as a one-rank loopback on `device` --
+// a communicator of size 1 (ncclCommInitRank), one grouped ncclSend / ncclRecv
+// pair to itself of `count` real elements of `dtype` (the PAIRWISE exchange
+// above), one ncclAlltoAll (the COLLECTIVE exchange; skipped when the loaded
+// NCCL lacks it), the one-int ncclAllReduce of the peer-store barrier and the
+// async-error poll, all through the dlopen'ed function table.  Received data
+// must equal what was sent.  NCCL refuses two ranks on one GPU, so on a
+// one-GPU box this is as much of the NCCL path as can execute.
+int tffft_nccl_loopback(int device, long long count, int dtype, int* ran_alltoall) {
+  if (count < 1 || (dtype != TFFFT_F64 && dtype != TFFFT_F32))
+    return fail(TFFFT_ERR_CONFIGURATION, "nccl_loopback: count %lld, dtype %d", count, dtype);
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(TFFFT_ERR_TRANSPORT, "NCCL unavailable: %s", api.err.c_str());
+  CUDA_TRY(cudaSetDevice(device));
+  const size_t rb = dtype == TFFFT_F64 ? 8 : 4, bytes = (size_t)count * rb;
+  const ncclDataType_t dt = dtype == TFFFT_F64 ? ncclFloat64 : ncclFloat32;
+  ncclUniqueId uid;
+  NCCL_TRY(api.GetUniqueId(&uid));
+  ncclComm_t comm = nullptr;
+  NCCL_TRY(api.CommInitRank(&comm, 1, uid, 0));
+  std::vector<unsigned char> h(bytes), back(bytes);
+  for (size_t i = 0; i < bytes; ++i) h[i] = (unsigned char)((i * 2654435761u) >> 13);
+  if (dtype == TFFFT_F64) {  // finite values: clear the exponent's top bits
+    for (size_t i = 7; i < bytes; i += 8) h[i] &= 0x3f;
+  } else {
+    for (size_t i = 3; i < bytes; i += 4) h[i] &= 0x3f;
+  }
+  void *src = nullptr, *dst = nullptr, *dst2 = nullptr;
+  int* flag = nullptr;
+  cudaStream_t s = nullptr;
+  int rc = TFFFT_OK;
+  auto cleanup = [&] {
+    if (s) cudaStreamDestroy(s);
+    cudaFree(src); cudaFree(dst); cudaFree(dst2); cudaFree(flag);
+    if (comm) api.CommDestroy(comm);
+  };
+#define LB_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      rc = fail(TFFFT_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));             \
+      cleanup();                                                                             \
+      return rc;                                                                             \
+    }                                                                                        \
+  } while (0)
+#define LB_NCCL(expr)                                                                        \
+  do {                                                                                       \
+    ncclResult_t _r = (expr);                                                                \
+    if (_r != ncclSuccess) {                                                                 \
+      rc = fail(TFFFT_ERR_TRANSPORT, "%s failed: %s", #expr, api.GetErrorString(_r));        \
+      cleanup();                                                                             \
+      return rc;                                                                             \
+    }                                                                                        \
+  } while (0)
+  LB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  LB_CUDA(cudaMalloc(&src, bytes));
+  LB_CUDA(cudaMalloc(&dst, bytes));
+  LB_CUDA(cudaMalloc(&dst2, bytes));
+  LB_CUDA(cudaMalloc(&flag, sizeof(int)));
+  LB_CUDA(cudaMemcpyAsync(src, h.data(), bytes, cudaMemcpyHostToDevice, s));
+  LB_CUDA(cudaMemsetAsync(dst, 0xFF, bytes, s));
+  LB_CUDA(cudaMemsetAsync(dst2, 0xFF, bytes, s));
+  LB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  LB_NCCL(api.GroupStart());
+  LB_NCCL(api.Send(src, (size_t)count, dt, 0, comm, s));
+  LB_NCCL(api.Recv(dst, (size_t)count, dt, 0, comm, s));
+  LB_NCCL(api.GroupEnd());
+  if (api.AlltoAll) LB_NCCL(api.AlltoAll(src, dst2, (size_t)count, dt, comm, s));
+  LB_NCCL(api.AllReduce(flag, flag, 1, ncclInt32, ncclSum, comm, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  ncclResult_t async_err = ncclSuccess;
+  LB_NCCL(api.CommGetAsyncError(comm, &async_err));
+  LB_NCCL(async_err);
+  LB_CUDA(cudaMemcpy(back.data(), dst, bytes, cudaMemcpyDeviceToHost));
+  if (memcmp(back.data(), h.data(), bytes) != 0) {
+    rc = fail(TFFFT_ERR_TRANSPORT, "nccl_loopback: send/recv payload differs");
+    cleanup();
+    return rc;
+  }
+  if (api.AlltoAll) {
+    LB_CUDA(cudaMemcpy(back.data(), dst2, bytes, cudaMemcpyDeviceToHost));
+    if (memcmp(back.data(), h.data(), bytes) != 0) {
+      rc = fail(TFFFT_ERR_TRANSPORT, "nccl_loopback: all-to-all payload differs");
+      cleanup();
+      return rc;
+    }
+  }
+#undef LB_CUDA
+#undef LB_NCCL
+  if (ran_alltoall) *ran_alltoall = api.AlltoAll ? 1 : 0;
+  cleanup();
+  return TFFFT_OK;
+}
+
 int tffft_plan_batch(tffft_plan_t pl, int* batch) {
   if (!pl || !batch) return fail(TFFFT_ERR_CONFIGURATION, "null argument");
   *batch = pl->batch;

@@ -41,6 +41,7 @@ __all__ = [
     "make_communicators",
     "run_spmd",
     "init_nccl_endpoint",
+    "nccl_loopback",
     "init_ipc_endpoint",
     "allgather_handles",
 ]
@@ -186,6 +187,18 @@ def run_spmd(p: int, fn, mode: CommMode = CommMode.THREADED, device: int | None 
     if primary is not None:
         raise primary
     return results
+
+
+def nccl_loopback(device: int = 0, count: int = 1 << 20, dtype: str = "float64") -> bool:
+    """Run the exchange's NCCL calls as a one-rank loopback on ``device``
+    (``tffft_nccl_loopback``): grouped send/recv to self, all-to-all, the
+    one-int all-reduce barrier.  Returns whether the loaded NCCL had
+    ``ncclAlltoAll``; raises ``TransportError`` when a call or the payload
+    comparison fails."""
+    ran = ctypes.c_int(0)
+    _lib.check(_lib.lib().tffft_nccl_loopback(int(device), int(count), 0 if dtype == "float64" else 1,
+                                              ctypes.byref(ran)))
+    return bool(ran.value)
 
 
 def init_nccl_endpoint(device: int | None = None) -> Endpoint:

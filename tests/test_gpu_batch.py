@@ -209,3 +209,22 @@ def test_deferred_consistency_mode():
     with pytest.raises(tf.ConsistencyError):
         tf.inverse(fp, spec)
     fp.close()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_nccl_calls_one_rank_loopback(dtype):
+    """The exchange's NCCL calls through the dlopen'ed function table, as far as
+    a one-GPU box can execute them (NCCL refuses two ranks on one device): a
+    one-rank communicator, a grouped ncclSend / ncclRecv to self of one
+    1024^3 p = 8 band chunk's worth of elements, ncclAlltoAll when the loaded
+    NCCL has it, the one-int ncclAllReduce of the peer-store barrier and the
+    async-error poll; the received payload must equal the sent one
+    (tffft_nccl_loopback; exchange.py:263-290 over transport.py:359-419)."""
+    count = 2 * 128 * 513 * 16  # real words of 16 planes of a 1024^3 p = 8 band
+    try:
+        ran_alltoall = tf.nccl_loopback(0, count, dtype)
+    except tf.TransportError as e:
+        if "NCCL unavailable" in str(e):
+            pytest.skip(str(e))
+        raise
+    assert ran_alltoall in (True, False)
