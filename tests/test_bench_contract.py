@@ -61,6 +61,30 @@ def test_gpus_n_without_torchrun_self_launches(monkeypatch):
     assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
 
 
+def test_stage3_kernel_name_follows_the_library_defaults(monkeypatch):
+    """roofline.kernel names the stage-3 kernel libtffft runs by default
+    (columns_wpc / columns_tma in csrc/tffft.cu): float64 1024-point columns
+    keep col_tma_kernel, 512-point / float32 1024-point columns the
+    warp-per-column kernel, 2048-point columns its tensor-memory 2 x 1024
+    variant, other lengths col_fft_kernel; TFFFT_WPC / TFFFT_TMA_COLS override."""
+    import bench
+
+    monkeypatch.delenv("TFFFT_WPC", raising=False)
+    monkeypatch.delenv("TFFFT_TMA_COLS", raising=False)
+    assert bench.stage3_kernel_name(1024, "float64") == "col_tma_kernel"
+    assert bench.stage3_kernel_name(1024, "float32") == "col_wpc_kernel"
+    assert bench.stage3_kernel_name(512, "float64") == "col_wpc_kernel"
+    assert bench.stage3_kernel_name(2048, "float64") == "col_wpc2_kernel"
+    assert bench.stage3_kernel_name(256, "float64") == "col_fft_kernel"
+    monkeypatch.setenv("TFFFT_WPC", "1")
+    assert bench.stage3_kernel_name(1024, "float64") == "col_wpc_kernel"
+    monkeypatch.setenv("TFFFT_WPC", "0")
+    assert bench.stage3_kernel_name(512, "float64") == "col_tma_kernel"
+    assert bench.stage3_kernel_name(2048, "float64") == "col_fft_kernel"
+    monkeypatch.setenv("TFFFT_TMA_COLS", "0")
+    assert bench.stage3_kernel_name(1024, "float64") == "col_fft_kernel"
+
+
 @pytest.mark.gpu
 def test_gpu_arm_line():
     """The GPU arm at a small grid: device-timed value, roofline with the
