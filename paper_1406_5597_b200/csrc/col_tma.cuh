@@ -34,11 +34,18 @@
 // (exchange.py:114-121) applied by the FFT's own TMA boxes and stores.
 //
 // Measured on 1024^3 (profiles/r01s10/tma_f64_ticket.txt, r01s11/tma_512.txt):
-// with the ticket tile order the TMA kernel is the default for every 512- and
+// with the ticket tile order this kernel beat col_fft_kernel on every 512- and
 // 1024-point column pass of either precision (2.96 ms per float64 1024^3
-// launch against 3.25-3.69 ms for col_fft_kernel).  Storing half of each tile
-// through the TMA unit as well (staged behind the next tile's boxes in the
-// exchange buffer) did not change the time.
+// launch against 3.25-3.69 ms).  Storing half of each tile through the TMA
+// unit as well (staged behind the next tile's boxes in the exchange buffer)
+// did not change the time.
+//
+// Since round 2 session 4 the warp-per-column kernels (col_wpc.cuh,
+// col_wpc2.cuh) run most of those passes (tffft.cu columns_wpc).  This kernel
+// keeps the float64 1024-point stage-3 / 3' passes (a tie in isolation, faster
+// live, profiles/r02s4/wpc_ab.txt), the float32 stage-1b rows that miss
+// 16-byte alignment on odd rows (the two-map parity scheme below; a swizzled
+// box cannot start off alignment), and anything TFFFT_WPC=0 sends back.
 #pragma once
 #include <cuda.h>
 
