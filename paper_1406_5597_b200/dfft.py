@@ -165,9 +165,10 @@ def plan(grid: GlobalGrid, comm: Endpoint, strategy: Strategy = Strategy.STRIDED
     ``algorithms`` selects optional kernel schedules ("fused_stage1",
     "fourstep_stage3", "peer_stores", "tma_columns", "chunked_exchange");
     None takes the library
-    defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS environment
-    switches; by default the 512- and 1024-point column passes at p = 1 are
-    TMA-fed).  ``batch`` > 1 makes a batched plan: ``forward_many`` /
+    defaults (TFFFT_FUSE / TFFFT_FOURSTEP / TFFFT_TMA_COLS / TFFFT_WPC
+    environment switches; by default the 512-, 1024- and 2048-point column
+    passes are TMA-fed at any p: the warp-per-column kernels or
+    col_tma_kernel).  ``batch`` > 1 makes a batched plan: ``forward_many`` /
     ``inverse_many`` transform ``batch`` fields per call (one launch per stage
     over all fields at p = 1; field c's exchange overlapping field c+1's
     compute at p > 1)."""
