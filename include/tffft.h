@@ -116,6 +116,8 @@ enum {
                                      exchange reduces to a barrier.  Local fabric communicators. */
   TFFFT_FLAG_CHUNKED_EXCHANGE = 32, /* p > 1 forward: stage 1 in plane chunks, each chunk's part of every band
                                      exchanged (on the plan's exchange stream) while the next chunk computes;
+                                     inverse: the bands exchanged plane chunk after plane chunk, stage 1' of a
+                                     chunk running as soon as it has landed;
                                      the default on NCCL communicators (TFFFT_XCHUNKS chunks, default 4),
                                      opt-in on the local fabric and IPC */
   TFFFT_FLAG_TMA_COLUMNS = 16     /* column passes of length 512 / 1024 / 2048 fed by TMA box copies: the

@@ -278,7 +278,7 @@ struct tffft_plan_s {
   BufSet bs[2];
   int nsets = 1;
   int cur = 0;               // the set the stage launchers address
-  int xchunks = 1;           // plane chunks of the chunked forward exchange (1 = one exchange per call)
+  int xchunks = 1;           // plane chunks of the chunked exchange, both directions (1 = one exchange per call)
   bool peer_stores = false;  // epilogues store peer bands straight into the peers' landing buffers
   bool peer_stores_wanted = false;  // NCCL communicator: peer stores once the peers' landing buffers are attached
   std::vector<void*> ipc_opened;    // peer mappings opened through CUDA IPC (closed at destroy)
@@ -546,7 +546,8 @@ static int stage1_columns(tffft_plan_t pl, void* spec, bool inv, cudaStream_t s,
       for (void* d : B.band_dst_h) j.st_tab.push_back(static_cast<char*>(d) + (size_t)plane0 * n1p * n2c * pl->esz);
       j.st_rows = n1p; j.st_in = n2c; j.st_g = n1p * n2c;
     } else {
-      j.ld_base = B.landing; j.ld_in_rows = n1p; j.ld_blocks = pl->p; j.ld_in = n2c; j.ld_out = band;
+      j.ld_base = static_cast<char*>(B.landing) + (size_t)plane0 * n1p * n2c * pl->esz;
+      j.ld_in_rows = n1p; j.ld_blocks = pl->p; j.ld_in = n2c; j.ld_out = band;
       j.ld_g = n1p * n2c;
       j.st_base = spec; j.st_rows = pl->n1; j.st_in = n2c; j.st_g = (long long)pl->n1 * n2c;
     }
@@ -1226,6 +1227,12 @@ static int exchange(tffft_plan_t pl, cudaStream_t s, long long i0 = 0, long long
     }
     // one send and one receive per peer (the plane range of each band is contiguous)
     const long long off = i0 * chunk * pl->esz, count = 2 * ni * chunk;
+    if (pl->pattern == TFFFT_COLLECTIVE && api.AlltoAll) {
+      // COLLECTIVE plans keep the self band in the all-to-all's self slot (build_band_dst); a plane
+      // chunk goes through send / recv instead, so the self band's chunk moves with a device copy
+      const long long so = (long long)pl->rank * band * pl->esz + off;
+      CUDA_TRY(cudaMemcpyAsync(lnd + so, stg + so, (size_t)(ni * chunk * pl->esz), cudaMemcpyDeviceToDevice, s));
+    }
     NCCL_TRY(api.GroupStart());
     for (int d = 1; d < pl->p; ++d) {
       const int to = (pl->rank + d) % pl->p, from = (pl->rank - d + pl->p) % pl->p;
@@ -2161,6 +2168,44 @@ static int pipeline(tffft_plan_t pl, cudaStream_t s, Produce produce, Consume co
 
 }  // extern "C++"
 
+// Chunked inverse at p > 1 (one field, component c of the batch): stage 3'
+// writes every band, then the bands are exchanged plane chunk after plane
+// chunk on the exchange stream x, and stage 1' (n1 columns + c2r rows) of
+// chunk k runs on the caller's stream s as soon as that chunk has landed, so
+// it overlaps the transfer of chunk k+1 -- the mirror of forward_chunked (the
+// consuming stage, not the producing one, hides the exchange here: a column
+// of stage 3' feeds every plane, while a plane of stage 1' needs one chunk).
+static int inverse_chunked(tffft_plan_t pl, void* spec, void* real, int c, cudaStream_t s, StageEvents* ev) {
+  cudaStream_t x = pl->xstream;
+  pl->cur = 0;
+  TRY(guard_outgoing(pl, s));
+  {
+    NvtxRange r("stage3");
+    TRY(stage3_columns(pl, spec, true, s));
+  }
+  MARK(ev, 1, s);
+  CUDA_TRY(cudaEventRecord(pl->ev_s1[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(x, pl->ev_s1[0], 0));
+  const int C = pl->xchunks, m = (pl->n0p + C - 1) / C;
+  const size_t rb = (size_t)pl->n1 * pl->n2 * (pl->esz / 2), sb = (size_t)pl->n1 * pl->n2c * pl->esz;
+  {
+    NvtxRange r("exchange+stage1");
+    for (int a = 0, k = 0; a < pl->n0p; a += m, ++k) {
+      const int cnt = std::min(m, pl->n0p - a);
+      TRY(exchange(pl, x, a, cnt));
+      CUDA_TRY(cudaEventRecord(pl->ev_x[k & 1], x));
+      CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_x[k & 1], 0));
+      char* sp = static_cast<char*>(spec) + (size_t)a * sb;
+      TRY(stage1_columns(pl, sp, true, s, cnt, a));
+      CUDA_TRY(c2r_launch(pl, row_params(pl, static_cast<char*>(real) + (size_t)a * rb, sp, cnt,
+                                         (long long)c * pl->n0p + a), s));
+    }
+  }
+  MARK(ev, 2, s);
+  MARK(ev, 3, s);
+  return TFFFT_OK;
+}
+
 int tffft_forward(tffft_plan_t pl, const void* real_in, void* spec_out, void* stream) {
   if (!pl) return fail(TFFFT_ERR_CONFIGURATION, "null plan");
   TRY(check_ptr(real_in, "real_in", pl->esz));
@@ -2222,7 +2267,10 @@ int tffft_inverse(tffft_plan_t pl, void* spec_inout, void* real_out, void* strea
       StageEvents* ev;
       TRY(begin_events(pl, false, s, &ev));
       pl->cur = 0;
-      TRY(inverse_field(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), 1, c, s, ev));
+      if (pl->xchunks > 1 && !pl->peer_stores && pl->strategy == 0 && !pl->s1_fused)
+        TRY(inverse_chunked(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), c, s, ev));
+      else
+        TRY(inverse_field(pl, spec + c * spec_bytes(pl), real + c * real_bytes(pl), 1, c, s, ev));
     }
   } else {
     StageEvents* ev;

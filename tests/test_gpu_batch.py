@@ -153,32 +153,45 @@ def test_comm_init_all_single_device():
 
 @pytest.mark.parametrize("p", [2, 4, 8])
 @pytest.mark.parametrize("pattern", [tf.CommPattern.PAIRWISE, tf.CommPattern.COLLECTIVE])
-def test_chunked_forward_exchange(p, pattern):
-    """Plane-chunked forward (TFFFT_FLAG_CHUNKED_EXCHANGE): stage 1 in plane
-    chunks, each chunk's share of every band exchanged on the exchange stream
-    while the next chunk computes; same spectra as the unchunked forward, the
-    same wire bytes."""
-    shape = (1024, 64, 16)
+@pytest.mark.parametrize("shape", [(1024, 64, 16), (32, 1024, 16)], ids=lambda v: "x".join(map(str, v)))
+def test_chunked_exchange_both_directions(p, pattern, shape):
+    """Plane-chunked exchange (TFFFT_FLAG_CHUNKED_EXCHANGE).  Forward: stage 1
+    in plane chunks, each chunk's share of every band exchanged on the
+    exchange stream while the next chunk computes.  Inverse: the bands are
+    exchanged plane chunk after plane chunk and stage 1' (n1 columns + c2r
+    rows) of a chunk runs as soon as it has landed, overlapping the next
+    chunk's transfer.  Same spectra and real fields, bit for bit, as the
+    unchunked plan, and the same wire bytes; (32, 1024, 16) puts the two-level
+    warp-per-column kernel on the chunked n1 passes (plane offsets into the
+    band tables and the landing buffer)."""
     x = oracle.uniform_field(shape, seed=7)
     grid = tf.GlobalGrid(*shape)
     slabs = tf.scatter_real(x, grid, p)
 
     def body(ep):
-        fp = tf.plan(grid, ep, comm_pattern=pattern, algorithms=("chunked_exchange", "tma_columns"))
-        assert "chunked_exchange" in fp.algorithms
-        spec = tf.forward(fp, slabs[ep.rank]).data.cpu().numpy().copy()
-        wire = fp.counters.bytes_wire
-        back = tf.inverse(fp, tf.forward(fp, slabs[ep.rank])).data.cpu().numpy().copy()
-        fp.close()
-        return spec, back, wire
+        out = []
+        for algs in (("tma_columns",), ("chunked_exchange", "tma_columns")):
+            fp = tf.plan(grid, ep, comm_pattern=pattern, algorithms=algs)
+            assert ("chunked_exchange" in fp.algorithms) == ("chunked_exchange" in algs)
+            spec = tf.forward(fp, slabs[ep.rank]).data.cpu().numpy().copy()
+            wire_f = fp.counters.bytes_wire
+            back = tf.inverse(fp, tf.forward(fp, slabs[ep.rank])).data.cpu().numpy().copy()
+            wire = fp.counters.bytes_wire
+            fp.close()
+            out.append((spec, back, wire_f, wire))
+        return out
 
     res = tf.run_spmd(p, body)
     ref = oracle.forward_all(x, p)
     n0p, n1p, n2c = shape[0] // p, shape[1] // p, shape[2] // 2 + 1
+    band_bytes = (p - 1) * n0p * n1p * n2c * 16
     for q in range(p):
-        assert rel(res[q][0], ref[q]) <= 1e-12
-        assert res[q][2] == (p - 1) * n0p * n1p * n2c * 16
-    back = np.concatenate([r[1] for r in res]).reshape(shape)
+        plain, chunked = res[q]
+        assert rel(chunked[0], ref[q]) <= 1e-12
+        assert np.array_equal(chunked[0], plain[0]) and np.array_equal(chunked[1], plain[1])
+        assert chunked[2] == band_bytes and chunked[3] == 3 * band_bytes  # forward, forward, inverse
+        assert plain[3] == 3 * band_bytes
+    back = np.concatenate([r[1][1] for r in res]).reshape(shape)
     assert rel(back, x) <= 1e-12
 
 
