@@ -39,6 +39,10 @@ CASES = [
     ((32, 1024, 16), 4, {}),                                             # warp-per-column two-level stage 1b
     ((32, 1024, 16), 8, {"algorithms": ("peer_stores", "tma_columns")}),  # ... storing into the peers' landing
     ((32, 1024, 16), 2, {"batch": 3}),                                   # ... in the batched pipeline
+    ((2048, 32, 16), 1, {}),                                             # 2 x 1024 tensor-memory kernel, stage 3
+    ((16, 2048, 32), 4, {}),                                             # ... two-level stage 1b (5D landing loads)
+    ((2048, 32, 16), 2, {"algorithms": ("chunked_exchange", "tma_columns")}),  # ... with the chunked exchange
+    ((512, 64, 16), 4, {"algorithms": ("chunked_exchange", "tma_columns")}),   # chunked, both directions, 512 points
 ]
 
 
