@@ -647,6 +647,9 @@ static int columns_wpc(tffft_plan_t pl, int L, bool inv, const TwoLevelJob& j, c
   const long long B = pl->dtype == TFFFT_F64 ? col_wpc_width<double>(L) : col_wpc_width<float>(L);
   const bool two = !j.st_tab.empty();
   if (B <= 0 || j.ld_in_rows * j.ld_blocks != n || (int)j.st_tab.size() > kWpcMaps) return TFFFT_OK;
+  // a TMA store writes whole 16-byte chunks: an odd number of float32 columns would spill 8 bytes past the
+  // last column of every row (DESIGN finding 34)
+  if ((j.cols * esz) % 16) return TFFFT_OK;
   if ((j.ld_in * esz) % 16 || (j.ld_blocks > 1 && (j.ld_out * esz) % 16) || (j.ngrp > 1 && (j.ld_g * esz) % 16) ||
       reinterpret_cast<uintptr_t>(j.ld_base) % 16 || (j.st_in * esz) % 16 || (j.ngrp > 1 && (j.st_g * esz) % 16))
     return TFFFT_OK;

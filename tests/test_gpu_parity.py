@@ -429,7 +429,10 @@ WPC_CASES = [((1024, 16, 8), 1), ((8, 1024, 16), 1), ((1024, 1024, 4), 1), ((16,
              ((32, 1024, 16), 2), ((32, 1024, 16), 4), ((64, 1024, 16), 8), ((16, 1024, 8), 16),
              ((1024, 64, 16), 2), ((1024, 32, 16), 8),
              ((512, 16, 8), 1), ((8, 512, 16), 1), ((512, 512, 8), 1), ((32, 512, 16), 4), ((512, 64, 16), 2),
-             ((512, 32, 16), 8), ((16, 512, 8), 16)]
+             ((512, 32, 16), 8), ((16, 512, 8), 16),
+             # one spectral row per rank (n1p = 1): an odd number of columns per rank, which the float32
+             # TMA stores must not take (whole 16-byte chunks)
+             ((1024, 2, 4), 2), ((512, 4, 8), 4)]
 
 
 @pytest.mark.parametrize("shape,p", WPC_CASES, ids=lambda v: str(v))
@@ -479,7 +482,7 @@ def test_wpc_column_kernel_bitwise(shape, p, dtype, monkeypatch):
 
 WPC2_CASES = [((2048, 16, 8), 1), ((8, 2048, 16), 1), ((2048, 2048, 4), 1), ((16, 2048, 64), 1),
               ((2048, 32, 16), 2), ((32, 2048, 16), 4), ((2048, 2048, 2), 8), ((64, 2048, 8), 16),
-              ((2048, 64, 4), 64)]
+              ((2048, 64, 4), 64), ((2048, 2, 4), 2)]
 
 
 @pytest.mark.parametrize("shape,p", WPC2_CASES, ids=lambda v: str(v))
