@@ -12,7 +12,7 @@ q's buffer is oracle.scatter_spectral(G, p)[q].
 Configs (BASELINE.json): 512^3 float64 standard normal at p = 1, 2, 4 (p > 1
 on the local fabric: p ranks on one GPU); 1024^3 float64 and float32 uniform
 at p = 1 (the headline bench configuration; float32 gets the fp32-rounded
-input); the turbulence field (3 components, inverse
+input) and float64 at p = 8 on the local fabric; the turbulence field (3 components, inverse
 then forward) at 256^3 for p = 1, 2; and the per-rank shapes of 2048^3
 over 8 ranks (config 4, which does not fit one GPU as a whole): 256 x 2048 x
 2048 (rows of 2048, n1 = 2048 columns) and 2048 x 256 x 2048 (n0 = 2048
@@ -92,6 +92,35 @@ def test_1024_cubed_p1_vs_oracle(dtype):
     fp.close()
     assert e_fwd <= TOL[dtype], e_fwd
     assert e_rt <= TOL[dtype], e_rt
+
+
+def test_1024_cubed_p8_local_fabric_vs_oracle():
+    """The headline grid split over 8 ranks (local fabric: eight ranks on one
+    B200), every rank's STRIDED_INPLACE buffer against the oracle's p = 1
+    spectrum scattered to 8 ranks (the reference is bitwise p-invariant), and
+    the round trip: the two-level column kernels, the band-redirecting stage
+    1b and the exchange at the size north_star names for 8 GPUs."""
+    shape, p = (1024, 1024, 1024), 8
+    x = oracle.uniform_field(shape, seed=11)
+    G = oracle.forward_all(x, 1, workers=WORKERS)[0].reshape(1024, 1024, 513)
+    grid = tf.GlobalGrid(*shape)
+    slabs = tf.scatter_real(x, grid, p)
+    del x
+    refs = oracle.scatter_spectral(G, p)
+    del G
+
+    def body(ep):
+        fp = tf.plan(grid, ep, tf.Strategy.STRIDED)
+        spec = tf.forward(fp, slabs[ep.rank])
+        e_fwd = rel_dev(spec.data, refs[ep.rank])
+        back = tf.inverse(fp, spec)
+        e_rt = rel_dev(back.data, slabs[ep.rank].data)
+        fp.close()
+        return e_fwd, e_rt
+
+    res = tf.run_spmd(p, body)
+    for e_fwd, e_rt in res:
+        assert e_fwd <= 1e-12 and e_rt <= 1e-12, res
 
 
 @pytest.mark.parametrize("shape", [(256, 2048, 2048), (2048, 256, 2048)], ids=lambda v: "x".join(map(str, v)))
