@@ -173,12 +173,13 @@ template <typename T, int L, bool WIDE = false> struct ColCfg {
 #ifndef TFFFT_R2C_MINB9
 #define TFFFT_R2C_MINB9 8
 #endif
-// (c2r at 5 CTAs/SM: 3.44 -> 3.34 ms per 256x2048x2048 launch, profiles/r02s4/rows_2048.txt)
+// (radix 16 x 8 x 8, E = 16, at 4 CTAs/SM of 128 threads -- 128 registers: r2c 2.88 -> 2.71 ms, c2r
+// 3.04 -> 2.95 ms per 256x2048x2048 launch; 5 CTAs/SM spills: c2r 3.74 ms; profiles/r02s4/rows_2048.txt)
 #ifndef TFFFT_C2R_MINB10
-#define TFFFT_C2R_MINB10 5
+#define TFFFT_C2R_MINB10 4
 #endif
 #ifndef TFFFT_R2C_MINB10
-#define TFFFT_R2C_MINB10 1
+#define TFFFT_R2C_MINB10 4
 #endif
 // r2c row schedule: float64 rows of n2 = 1024 run the radix-8 schedule
 // (3 passes, E = 8, 6 CTAs/SM: 3.10 ms per 1024^3 launch vs 3.62 ms with radix
@@ -224,8 +225,8 @@ template <int L, int MB = 0> struct RowCfg {
   // pair loads -- at 5 (94 registers, 2.88 ms).  Other lengths keep the default.
   // (radix-8 schedule only, E = 8; the radix-32 schedule needs ~200 registers)
   static constexpr bool CAP = (L == 9 || L == 8) && THREADS == 128 && Shape<L, MB>::E == 8;
-  // n2 = 2048 on the radix-8 schedule (E = 8, one row per 128-thread CTA): TFFFT_R2C_MINB10 / TFFFT_C2R_MINB10
-  static constexpr bool CAP10 = L == 10 && THREADS == 128 && Shape<L, MB>::E == 8;
+  // n2 = 2048 (E = 8 or 16, 128-thread CTAs): occupancy by launch bounds, TFFFT_R2C_MINB10 / TFFFT_C2R_MINB10
+  static constexpr bool CAP10 = L == 10 && THREADS == 128 && (Shape<L, MB>::E == 8 || Shape<L, MB>::E == 16);
   static constexpr int MINB_C2R = CAP ? TFFFT_C2R_MINB9 : (CAP10 ? TFFFT_C2R_MINB10 : TFFFT_ROW_MINB);
   static constexpr int MINB_R2C = CAP ? TFFFT_R2C_MINB9 : (CAP10 ? TFFFT_R2C_MINB10 : TFFFT_ROW_MINB);
 };
