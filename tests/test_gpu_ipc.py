@@ -44,6 +44,10 @@ CASES = [
     ((16, 1024, 8), "PAIRWISE", None, 1),
     ((64, 32, 16), "PAIRWISE", ("chunked_exchange", "tma_columns"), 1),
     ((64, 32, 16), "COLLECTIVE", ("chunked_exchange",), 1),
+    # warp-per-column kernels storing through tensor maps over IPC-mapped peer landing buffers
+    ((32, 1024, 16), "PAIRWISE", ("peer_stores", "tma_columns"), 1),   # stage 1b forward (1024 points)
+    ((2048, 16, 8), "PAIRWISE", ("peer_stores", "tma_columns"), 1),    # stage 3' (2 x 1024 through tensor memory)
+    ((512, 16, 8), "COLLECTIVE", ("peer_stores", "tma_columns"), 2),   # 512 points, batched pipeline
 ]
 
 
