@@ -24,6 +24,13 @@
 // a slot two rounds after its store was issued, so no warp waits for a store
 // that has only just been committed (with two 32 KB slots the consumers spent
 // 19% of their stall samples in that rendezvous, profiles/r02s4/wpc2_2048.txt).
+// Only the first eight rounds (X[k]) follow the combine directly: X[k + 1024]
+// is parked in a second tensor-memory region and drained after the NEXT half's
+// transform.  Both half-iterations then have the same length (one 1024-point
+// transform plus eight output rounds), so the landing ring is refilled at an
+// even pace instead of idling through sixteen rounds: 3.24 -> 2.93 ms per
+// 17.2 GB stage-1b launch, 3.25 -> 3.14 ms for stage 3.  All 512 tensor-memory
+// columns are in use (two regions of 128 KB).
 //
 // Loads go through a map with the row parity as its own dimension: (cols,
 // parity, half rows, groups), or at p > 1 (cols, parity, half rows within a
@@ -134,8 +141,10 @@ struct Wpc2Cfg {
   static constexpr int NH = 1024;                                 // points per half
   static constexpr int W8 = 2 * (int)sizeof(cx<T>);               // 32-bit words of 8 complex values
   static constexpr int NW = 4 * W8;                               // words a lane parks (32 values)
-  static constexpr int TCOLS = 256;                               // TMEM columns: (consumer warps / 4) x NW
-  static_assert((WC::B / 4) * NW == TCOLS, "tensor-memory columns");
+  static constexpr int TREG = 256;                                // TMEM columns of one region: (consumer warps / 4) x NW
+  static constexpr int TCOLS = 2 * TREG;                          // region A: E of this tile; region B: the second
+                                                                  // output half of the previous tile
+  static_assert((WC::B / 4) * NW == TREG, "tensor-memory columns");
   static constexpr size_t W2B = sizeof(cx<T>) * (size_t)NH;       // w^k, k < 1024
   static constexpr int NSLOT = 4, OROWS = 128;                    // output stage: slots of OROWS rows
   static constexpr size_t SLOTB = (size_t)OROWS * 128;
@@ -225,6 +234,36 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
     }
     for (int q = 0; q < NBOX; ++q) load_box(cur, 0, q);
     unsigned long long tk = 0;
+    unsigned pu[NSLOT] = {0, 0, 0, 0};  // uses of each output slot stored so far
+    // eight 128-row rounds of one tile: rows [128 (8 half + r), ...) through slots r & 3, each slot released two
+    // rounds after its store was issued
+    auto store_half = [&](long long tile, int half) {
+      const int grp = (int)(tile / prm.tpg), c0 = (int)(tile % prm.tpg) * B;
+#pragma unroll 1
+      for (int r8 = 0; r8 < NR / 2; ++r8) {
+        const int rr = half * (NR / 2) + r8, s = r8 & (NSLOT - 1);
+        mbar_wait(ofull + s, pu[s] & 1u);
+        ++pu[s];
+        const unsigned char* src = xs + (size_t)s * W2::SLOTB;
+        if (prm.nst > 1) {
+          const int smask = (1 << prm.sst_shift) - 1;
+          for (int r = rr * OROWS; r < (rr + 1) * OROWS; r += prm.sbrows)
+            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - rr * OROWS) * 128, pol);
+        } else {
+          tma_store3(&maps.st[0], 2 * c0, rr * OROWS, grp, src, pol);
+        }
+        bulk_commit();
+        if (r8 >= 2) {  // the store of two rounds ago has read its slot
+          bulk_wait_read2();
+          mbar_arrive(oempty + ((r8 - 2) & (NSLOT - 1)));
+        }
+      }
+      bulk_wait_read1();
+      mbar_arrive(oempty + ((NR / 2 - 2) & (NSLOT - 1)));
+      bulk_wait_read0();
+      mbar_arrive(oempty + ((NR / 2 - 1) & (NSLOT - 1)));
+    };
+    long long prev = -1;  // tile whose second output half is still parked in tensor memory
     for (unsigned it = 0;; ++it) {  // one iteration per half tile
       const unsigned par = it & 1u;
       const int h = (int)(it & 1u);
@@ -236,34 +275,17 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
         if (more) load_box(h == 0 ? cur : nxt, h ^ 1, q);
         else if (q == 0) mbar_arrive(full + 0);
       }
-      if (h == 0) continue;  // outputs exist after the odd half only
-      const int grp = (int)(cur / prm.tpg), c0 = (int)(cur % prm.tpg) * B;
-#pragma unroll 1
-      for (int rr = 0; rr < NR; ++rr) {
-        const int s = rr & (NSLOT - 1);
-        mbar_wait(ofull + s, (unsigned)((rr / NSLOT) & 1));  // slot s: NR / NSLOT (even) uses per tile
-        const unsigned char* src = xs + (size_t)s * W2::SLOTB;
-        if (prm.nst > 1) {
-          const int smask = (1 << prm.sst_shift) - 1;
-          for (int r = rr * OROWS; r < (rr + 1) * OROWS; r += prm.sbrows)
-            tma_store3(&maps.st[r >> prm.sst_shift], 2 * c0, r & smask, grp, src + (size_t)(r - rr * OROWS) * 128, pol);
-        } else {
-          tma_store3(&maps.st[0], 2 * c0, rr * OROWS, grp, src, pol);
-        }
-        bulk_commit();
-        if (rr >= 2) {  // the store of two rounds ago has read its slot
-          bulk_wait_read2();
-          mbar_arrive(oempty + ((rr - 2) & (NSLOT - 1)));
-        }
+      if (h == 0) {  // the consumers drain the previous tile's second half after this half's transform
+        if (prev >= 0) store_half(prev, 1);
+        continue;
       }
-      bulk_wait_read1();
-      mbar_arrive(oempty + ((NR - 2) & (NSLOT - 1)));
-      bulk_wait_read0();
-      mbar_arrive(oempty + ((NR - 1) & (NSLOT - 1)));
+      store_half(cur, 0);
+      prev = cur;
       if (!more) break;
       cur = nxt;
       nxt = dyn ? (long long)tk : nxt + step;
     }
+    store_half(prev, 1);  // drained by the consumers on their way out
     bulk_wait0();
     return;
   }
@@ -272,16 +294,36 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(WC::CREG));
   const int cchunk = (int)((w * sizeof(cx<T>)) >> 4) ^ (tt & 7);
   const int lane_ofs = tt * 128 + (cchunk << 4) + (int)((w * sizeof(cx<T>)) & 15);
-  // this lane's parking space: TMEM lane 32 (w % 4) + tt, NW columns from (w / 4) NW
+  // this lane's parking space: TMEM lane 32 (w % 4) + tt, NW columns from (w / 4) NW (region A), and the same
+  // columns of region B
   const uint32_t taddr = tbase + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * W2::NW);
+  const uint32_t taddr_b = taddr + W2::TREG;
   unsigned oe[NSLOT] = {0, 0, 0, 0};  // phases of oempty[s] consumed
-  unsigned g = 0;                     // uses of every slot begun in earlier tiles (use j is released by phase j + 1)
+  unsigned U = 0;                     // uses of every slot begun so far (use j is released by phase j + 1)
   auto need = [&](int s, unsigned phase) {  // slot s has been read out for every use before `phase`
     while (oe[s] <= phase) {
       mbar_wait(oempty + s, oe[s] & 1u);
       ++oe[s];
     }
   };
+  // the second output half of the previous tile, X[k + 1024], parked in region B: eight rounds to the stage
+  auto drain = [&] {
+    cx<T> d[8];
+#pragma unroll
+    for (int r8 = 0; r8 < NR / 2; ++r8) {
+      const int s = r8 & (NSLOT - 1);
+      need(s, U + r8 / NSLOT);
+      if (r8 % 2 == 0) tmem_fetch8<T>(taddr_b + (r8 / 2) * W2::W8, d);
+      unsigned char* ob = xs + (size_t)s * W2::SLOTB + lane_ofs;
+#pragma unroll
+      for (int k = 0; k < KPR; ++k) *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = d[(r8 % 2) * KPR + k];
+      fence_async_shared();
+      __syncwarp();
+      if (tt == 0) mbar_arrive(ofull + s);
+    }
+    U += NR / 2 / NSLOT;
+  };
+  bool pend = false;
   for (unsigned it = 0;; ++it) {
     const unsigned par = it & 1u;
     const int h = (int)(it & 1u);
@@ -301,46 +343,50 @@ col_wpc2_kernel(const __grid_constant__ WpcMaps maps, const WpcParams prm) {
     if (stop) break;
     ST::first(v, tt, s_tw);
 #pragma unroll
-    for (int s = 0; s < NSLOT; ++s) need(s, g);  // the exchange buffer doubles as the output stage
+    for (int s = 0; s < NSLOT; ++s) need(s, U);  // the exchange buffer doubles as the output stage
     auto hook = [&] {
       __syncwarp();
-      if (h == 1 && tt == 0) mbar_arrive(xdrained);
+      if (tt == 0) mbar_arrive(xdrained);
     };
     ST::finish(xs, v, tt, w, s_tw, hook);
-    if (h == 0) {  // E[tt + 32 m] waits in tensor memory
+    if (h == 0) {  // E[tt + 32 m] waits in region A
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_park8<T>(taddr + c * W2::W8, v + 8 * c);
       tmem_wait_st();
+      if (pend) {  // now the previous tile's second half, once every warp has left the exchange buffer
+        mbar_wait(xdrained, par);
+        drain();
+        pend = false;
+      }
       continue;
     }
-    mbar_wait(xdrained, (it >> 1) & 1u);
+    mbar_wait(xdrained, par);
     cx<T> e[8];
 #pragma unroll
-    for (int rr = 0; rr < NR; ++rr) {
+    for (int rr = 0; rr < NR / 2; ++rr) {  // rows tt + 32 m, m = KPR rr + k: X[k] = E + w^k O; E - w^k O goes to region B
       const int s = rr & (NSLOT - 1);
-      need(s, g + rr / NSLOT);
+      need(s, U + rr / NSLOT);
       unsigned char* ob = xs + (size_t)s * W2::SLOTB + lane_ofs;
-      if (rr < NR / 2) {  // rows tt + 32 m, m = KPR rr + k: X[k] = E + w^k O; keep E - w^k O for round rr + NR / 2
-        if (rr % 2 == 0) tmem_fetch8<T>(taddr + (rr / 2) * W2::W8, e);
+      if (rr % 2 == 0) tmem_fetch8<T>(taddr + (rr / 2) * W2::W8, e);
 #pragma unroll
-        for (int k = 0; k < KPR; ++k) {
-          const int m = rr * KPR + k;
-          const cx<T> ek = e[(rr % 2) * KPR + k];
-          const cx<T> tw = ctw<INV>(v[m], s_w2[tt + 32 * m]);
-          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = cadd(ek, tw);
-          v[m] = csub(ek, tw);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < KPR; ++k)
-          *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = v[(rr - NR / 2) * KPR + k];
+      for (int k = 0; k < KPR; ++k) {
+        const int m = rr * KPR + k;
+        const cx<T> ek = e[(rr % 2) * KPR + k];
+        const cx<T> tw = ctw<INV>(v[m], s_w2[tt + 32 * m]);
+        *reinterpret_cast<cx<T>*>(ob + (size_t)k * 32 * 128) = cadd(ek, tw);
+        v[m] = csub(ek, tw);
       }
       fence_async_shared();
       __syncwarp();
       if (tt == 0) mbar_arrive(ofull + s);
     }
-    g += NR / NSLOT;
+    U += NR / 2 / NSLOT;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_park8<T>(taddr_b + c * W2::W8, v + 8 * c);
+    tmem_wait_st();
+    pend = true;
   }
+  if (pend) drain();  // the last tile's second half (every warp left the exchange buffer long ago)
   // every consumer warp is done with tensor memory: warp 0 frees it
   tmem_fence_before();
   asm volatile("bar.sync 1, %0;" ::"n"(32 * WpcCfg<T, 10>::B) : "memory");
