@@ -6,6 +6,9 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+if os.environ.get("HUGE_ALLOC"):  # experiment: large buffers through tools/micro/libhugealloc.so (512 MB-aligned VMM mappings)
+    _so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "micro", "libhugealloc.so")
+    torch.cuda.memory.change_current_allocator(torch.cuda.memory.CUDAPluggableAllocator(_so, "huge_malloc", "huge_free"))
 import paper_1406_5597_b200 as tf
 
 ap = argparse.ArgumentParser()
