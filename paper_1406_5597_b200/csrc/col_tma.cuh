@@ -47,7 +47,6 @@
 // 16-byte alignment on odd rows (the two-map parity scheme below; a swizzled
 // box cannot start off alignment), and anything TFFFT_WPC=0 sends back.
 #pragma once
-#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include "fourstep_tma.cuh"
@@ -137,9 +136,6 @@ struct TmaColParams {
   void* tab[kTmaTab];    // TWO stores: block base pointers
   int tma_store;         // FPF, in place through `map` (parity 0): the first half of each output tile leaves
                          // through TMA boxes staged in the drained exchange buffer, the rest through STG
-  int cluster;           // > 1 (experiment, TFFFT_S3_CLUSTER): launched as clusters of this many CTAs that take
-                         // `cluster` consecutive tiles per ticket and issue their boxes behind one cluster
-                         // barrier, so the row visits of neighbouring tiles reach DRAM together
 };
 
 template <typename T, int L, bool INV, int NB, bool TWO, bool FPF>
@@ -186,21 +182,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
   const bool dyn = prm.ticket != nullptr;
   __shared__ long long s_tk[2];
   long long cur = blockIdx.x;
-  const int CL = prm.cluster > 1 ? prm.cluster : 1;
-  namespace cg = cooperative_groups;
-  const unsigned crank = CL > 1 ? cg::this_cluster().block_rank() : 0u;
-  if (CL > 1) {  // the leader's tickets, times CL, plus each member's rank (ntiles is a multiple of CL)
-    if (t == 0 && crank == 0) {
-      const long long a = (long long)atomicAdd(prm.ticket, 1ull), a2 = (long long)atomicAdd(prm.ticket, 1ull);
-      for (int r = 0; r < CL; ++r) {
-        long long* rs = cg::this_cluster().map_shared_rank(s_tk, r);
-        rs[1] = a * CL + r;
-        rs[0] = a2 * CL + r;
-      }
-    }
-    cg::this_cluster().sync();
-    cur = s_tk[1];
-  } else if (dyn) {
+  if (dyn) {
     if (t == 0) {
       cur = (long long)atomicAdd(prm.ticket, 1ull);
       s_tk[0] = (long long)atomicAdd(prm.ticket, 1ull);
@@ -247,7 +229,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     load_half(cur, 1);
   }
   for (long long i = 0; cur < prm.ntiles; ++i) {
-    long long nxt = CL > 1 ? 0 : (dyn ? s_tk[i & 1] : cur + step);
+    const long long nxt = dyn ? s_tk[i & 1] : cur + step;
     const unsigned par = (unsigned)(i & 1);
     mbar_wait(bar + 0, par);
     if (TC::NBOX > TC::NPF) mbar_wait(bar + 1, par);
@@ -256,15 +238,7 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
     for (int kk = 0; kk < E; ++kk) v[SH::in_slot(kk)] = operand(kk);
     // the previous tile's TMA store has read its staging (the exchange buffer)
     if (FPF && !TWO && t == 0 && prm.tma_store) bulk_wait_read0();
-    if (CL > 1) {
-      // every operand read in every CTA of the cluster; the leader's ticket
-      // store of the previous iteration is visible; the members' producer
-      // threads issue the next tiles' boxes together
-      cg::this_cluster().sync();
-      nxt = s_tk[i & 1];
-    } else {
-      __syncthreads();  // every operand read: both halves may be overwritten
-    }
+    __syncthreads();  // every operand read: both halves may be overwritten
     unsigned long long tk = 0;
     if (t == 0) {
       // the next tile's boxes first, then the ticket after next: its atomic
@@ -274,17 +248,10 @@ col_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ 
         load_half(nxt, 0);
         if (FPF) load_half(nxt, 1);
       }
-      if (dyn && crank == 0) tk = atomicAdd(prm.ticket, 1ull);
+      if (dyn) tk = atomicAdd(prm.ticket, 1ull);
     }
     ST::first(v, tt, s_tw);
-    if (CL > 1) {
-      // members read it after the next cluster barrier; none of them can have
-      // left while nxt is a tile (they all still owe that barrier)
-      if (t == 0 && crank == 0 && nxt < prm.ntiles)
-        for (int r = 0; r < CL; ++r) cg::this_cluster().map_shared_rank(s_tk, r)[(i + 1) & 1] = (long long)tk * CL + r;
-    } else if (t == 0 && dyn) {
-      s_tk[(i + 1) & 1] = (long long)tk;  // read next iteration, after the exchange barriers
-    }
+    if (t == 0 && dyn) s_tk[(i + 1) & 1] = (long long)tk;  // read next iteration, after the exchange barriers
     auto hook = [&] {  // the last exchange has drained the buffer
       if (!FPF && t == 0 && nxt < prm.ntiles) load_half(nxt, 1);
     };

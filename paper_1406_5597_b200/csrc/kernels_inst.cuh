@@ -284,27 +284,6 @@ static cudaError_t tc_one(const CUtensorMap& map, const CUtensorMap& map_odd, co
   const long long blocks =
       std::min<long long>(p.ntiles, (long long)occupancy(k, kc, TC::THREADS, TC::SMEM) * num_sms());
   (void)cudaGetLastError();
-  // experiment (TFFFT_S3_CLUSTER=C): clusters of C CTAs on C consecutive tiles per ticket, boxes issued
-  // behind a cluster barrier (col_tma.cuh `cluster`); wide in-place shape only
-  static const int cl = [] { const char* e = getenv("TFFFT_S3_CLUSTER"); return e ? atoi(e) : 1; }();
-  if (cl > 1 && cl <= 8 && !TWO && NB == tma_cols_per_cta<T, L>(true) && p.ticket && !p.tma_store &&
-      p.ntiles % cl == 0 && blocks / cl > 0) {
-    TmaColParams q = p;
-    q.cluster = cl;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(blocks / cl * cl));
-    cfg.blockDim = dim3(TC::THREADS);
-    cfg.dynamicSmemBytes = TC::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, map, map_odd, q);
-  }
   k<<<(unsigned)blocks, TC::THREADS, TC::SMEM, s>>>(map, map_odd, p);
   return cudaGetLastError();
   }
